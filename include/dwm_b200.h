@@ -1,0 +1,129 @@
+/*
+ * dwm_b200.h -- C ABI of the B200-native Decomposable Winograd (DWM) conv2d.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   dwmconv.engines.dwm_conv2d(data, weights, spec, plan=None,
+ *                              precision=None, counter=None)
+ *   (reference: pkg/src/dwmconv/engines.py:219-255)
+ * and the stages it runs.  The reference is pure Python/NumPy, so its
+ * "FFI" is the Python call itself; the Python package
+ * paper_2002_00552_b200 binds these symbols with ctypes
+ * (paper_2002_00552_b200/_native.py) and re-exposes the reference's exact
+ * signature.  INTEGRATION.md shows the ctypes stub a maintainer of the
+ * reference package would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every device pointer is CUDA global
+ *     memory; `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default stream).  All compute entry points are stream-ordered and
+ *     asynchronous; none synchronises the device.
+ *   - tensors are row-major NCHW (data, output) and F,C,r_h,r_w (weights),
+ *     exactly the reference's layouts.
+ *   - no hidden global mutable state except the thread-local error message
+ *     and the lazily-initialised per-device kernel attributes.
+ *   - every function returns a dwm_status; on failure dwm_last_error()
+ *     returns a human-readable message whose wording mirrors the
+ *     reference's ValueError/TypeError/FloatingPointError texts.
+ */
+#ifndef DWM_B200_H
+#define DWM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DWM_MAX_AXIS_PARTS 16
+
+typedef enum dwm_status {
+  DWM_OK = 0,
+  DWM_EINVAL_SHAPE = 1,   /* -> ValueError   (engines.py:66-68,231-236; convspec.py:23-43) */
+  DWM_EINVAL_DTYPE = 2,   /* -> TypeError    (tensor.py:18-23)                            */
+  DWM_NONFINITE = 3,      /* -> FloatingPointError (tensor.py:27-30)                       */
+  DWM_ECUDA = 4,          /* CUDA runtime failure                                          */
+  DWM_EUNSUPPORTED = 5    /* geometry outside what the kernels implement                   */
+} dwm_status;
+
+typedef enum dwm_dtype { DWM_F32 = 0, DWM_F64 = 1 } dwm_dtype;
+
+/* Transform-domain contraction engine.
+ *   EXACT: CUDA-core FMA chains in the reference's stage order (channel-
+ *          ascending GEMM, At.m.A row then column stage, plan-order part
+ *          sum).  Bit-identical to the reference where its BLAS accumulates
+ *          sequentially (small C); f32 and f64.
+ *   TC:    tcgen05/TMEM 3xTF32 GEMM with the output transform, part sum and
+ *          tile interleave fused in the epilogue (f32 only, C % 32 == 0,
+ *          F % 64 == 0).
+ *   AUTO:  TC when eligible and C is large enough to use it, else EXACT. */
+typedef enum dwm_algo { DWM_ALGO_AUTO = 0, DWM_ALGO_EXACT = 1, DWM_ALGO_TC = 2 } dwm_algo;
+
+/* One strided run of kernel taps along an axis: origin + step*i, i < count
+ * (reference AxisPart, decompose.py:25-35). */
+typedef struct dwm_axis_part {
+  int32_t origin, step, count;
+} dwm_axis_part_t;
+
+/* Geometry + decomposition plan.  Filled by dwm_desc_init() from the
+ * ConvSpec fields; the 2-D plan is the row-major cross product
+ * row_parts x col_parts (decompose.py:103-114). */
+typedef struct dwm_desc {
+  int32_t n, c, h, w, f;                      /* data N,C,H,W; filters F    */
+  int32_t r_h, r_w, s_h, s_w;                 /* kernel taps, stride        */
+  int32_t pad_top, pad_bottom, pad_left, pad_right;
+  /* derived */
+  int32_t oh, ow;                             /* convspec.py:34-44          */
+  int32_t th, tw;                             /* 2x2 output tiles per image */
+  int32_t n_row_parts, n_col_parts;
+  dwm_axis_part_t row_parts[DWM_MAX_AXIS_PARTS];
+  dwm_axis_part_t col_parts[DWM_MAX_AXIS_PARTS];
+  int32_t row_freqs, col_freqs;               /* sum of (count+1) per axis  */
+  int32_t num_freqs;                          /* sum over parts a_r*a_c     */
+  int64_t tiles;                              /* n * th * tw                */
+} dwm_desc_t;
+
+/* Plan a convolution: validates geometry exactly like ConvSpec/out_dims and
+ * runs the C++ restatement of plan_decomposition (decompose.py:60-114). */
+int dwm_desc_init(dwm_desc_t* desc, int n, int c, int h, int w, int f,
+                  int r_h, int r_w, int s_h, int s_w,
+                  int pad_top, int pad_bottom, int pad_left, int pad_right);
+
+/* FlopCounter increment of one call: TH*TW*sum_parts a_r*a_c
+ * (engines.py:190-191, == flops.flops_dwm, flops.py:107-119). */
+int64_t dwm_elementwise_count(const dwm_desc_t* desc);
+
+/* Bytes of caller-provided device workspace dwm_conv2d_forward needs. */
+size_t dwm_workspace_bytes(const dwm_desc_t* desc, int dtype, int algo);
+
+/* Resolve AUTO to the engine that will run (for reporting). */
+int dwm_select_algo(const dwm_desc_t* desc, int dtype, int algo);
+
+/* Stage kernels (exposed for the parity tests and the stage profiler).
+ *   U layout: [num_freqs][F][C]      (frequency order: parts in plan order,
+ *                                     row frequency, then column frequency)
+ *   V layout: [num_freqs][tiles][C]  (tile = (n*TH + ty)*TW + tx)        */
+int dwm_filter_transform(const dwm_desc_t* desc, int dtype, const void* w,
+                         void* U, void* stream);
+int dwm_input_transform(const dwm_desc_t* desc, int dtype, const void* x,
+                        void* V, void* stream);
+int dwm_gemm_output(const dwm_desc_t* desc, int dtype, int algo, const void* V,
+                    const void* U, void* y, int32_t* nonfinite_flag,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Whole forward: y[N,F,OH,OW] = dwm_conv2d(x[N,C,H,W], w[F,C,r_h,r_w]).
+ * nonfinite_flag (device int32, may be NULL) is set to 1 when any output
+ * is NaN/Inf; the caller raises FloatingPointError after syncing. */
+int dwm_conv2d_forward(const dwm_desc_t* desc, int dtype, int algo,
+                       const void* x, const void* w, void* y,
+                       void* workspace, size_t workspace_bytes,
+                       int32_t* nonfinite_flag, void* stream);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* dwm_last_error(void);
+const char* dwm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DWM_B200_H */

@@ -1,0 +1,184 @@
+// dwm_capi.cu -- C ABI: planner, validation, workspace sizing and dispatch.
+//
+// The planner is a C++ restatement of the reference's decompose.py:60-114
+// (stride-residue split, empty residues dropped, greedy blocks of 3 plus a
+// remainder, low taps first; 2-D plan = row-major cross product).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "dwm_common.cuh"
+#include "dwm_kernels.h"
+
+namespace dwm {
+
+static thread_local char g_err[512] = "";
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  return fail(DWM_ECUDA, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+              cudaGetErrorString(e), what, file, line);
+}
+
+// decompose.py:73-100 -- stride split, then size split of each residue run.
+static int plan_axis(int taps, int stride, dwm_axis_part_t* out, int* n_out) {
+  int n = 0;
+  for (int residue = 0; residue < stride; ++residue) {
+    const int run = (taps - residue + stride - 1) / stride;  // ceil, <= 0 if empty
+    if (run <= 0) continue;
+    int first = 0;
+    for (int left = run; left > 0;) {
+      const int block = left >= 3 ? 3 : left;
+      if (n >= DWM_MAX_AXIS_PARTS)
+        return fail(DWM_EUNSUPPORTED,
+                    "decomposition of %d taps at stride %d needs more than %d parts per axis",
+                    taps, stride, DWM_MAX_AXIS_PARTS);
+      out[n].origin = residue + stride * first;
+      out[n].step = stride;
+      out[n].count = block;
+      ++n;
+      first += block;
+      left -= block;
+    }
+  }
+  *n_out = n;
+  return DWM_OK;
+}
+
+}  // namespace dwm
+
+using namespace dwm;
+
+extern "C" {
+
+const char* dwm_last_error(void) { return g_err; }
+
+const char* dwm_version(void) { return "dwm_b200 0.1.0 (sm_100a)"; }
+
+int dwm_desc_init(dwm_desc_t* d, int n, int c, int h, int w, int f, int r_h, int r_w,
+                  int s_h, int s_w, int pad_top, int pad_bottom, int pad_left, int pad_right) {
+  if (!d) return fail(DWM_EINVAL_SHAPE, "descriptor pointer is NULL");
+  std::memset(d, 0, sizeof(*d));
+  // convspec.py:23-28
+  if (r_h < 1 || r_w < 1)
+    return fail(DWM_EINVAL_SHAPE, "kernel must be two positive integers, got (%d, %d)", r_h, r_w);
+  if (s_h < 1 || s_w < 1)
+    return fail(DWM_EINVAL_SHAPE, "stride must be two positive integers, got (%d, %d)", s_h, s_w);
+  if (pad_top < 0 || pad_bottom < 0 || pad_left < 0 || pad_right < 0)
+    return fail(DWM_EINVAL_SHAPE, "pad must be four non-negative integers, got (%d, %d, %d, %d)",
+                pad_top, pad_bottom, pad_left, pad_right);
+  if (n < 1 || c < 1 || h < 1 || w < 1 || f < 1)
+    return fail(DWM_EINVAL_SHAPE, "empty tensor: data (%d, %d, %d, %d), filters %d", n, c, h, w, f);
+  // convspec.py:34-44
+  const int oh = (h + pad_top + pad_bottom - r_h) / s_h + 1;
+  const int ow = (w + pad_left + pad_right - r_w) / s_w + 1;
+  if (h + pad_top + pad_bottom < r_h || w + pad_left + pad_right < r_w || oh < 1 || ow < 1)
+    return fail(DWM_EINVAL_SHAPE,
+                "input %dx%d with pad (%d, %d, %d, %d) is too small for kernel (%d, %d) stride (%d, %d)",
+                h, w, pad_top, pad_bottom, pad_left, pad_right, r_h, r_w, s_h, s_w);
+  d->n = n; d->c = c; d->h = h; d->w = w; d->f = f;
+  d->r_h = r_h; d->r_w = r_w; d->s_h = s_h; d->s_w = s_w;
+  d->pad_top = pad_top; d->pad_bottom = pad_bottom; d->pad_left = pad_left; d->pad_right = pad_right;
+  d->oh = oh; d->ow = ow;
+  d->th = (oh + 1) / 2; d->tw = (ow + 1) / 2;
+  int st = plan_axis(r_h, s_h, d->row_parts, &d->n_row_parts);
+  if (st) return st;
+  st = plan_axis(r_w, s_w, d->col_parts, &d->n_col_parts);
+  if (st) return st;
+  d->row_freqs = 0;
+  for (int i = 0; i < d->n_row_parts; ++i) d->row_freqs += d->row_parts[i].count + 1;
+  d->col_freqs = 0;
+  for (int i = 0; i < d->n_col_parts; ++i) d->col_freqs += d->col_parts[i].count + 1;
+  d->num_freqs = d->row_freqs * d->col_freqs;
+  d->tiles = (int64_t)n * d->th * d->tw;
+  return DWM_OK;
+}
+
+int64_t dwm_elementwise_count(const dwm_desc_t* d) {
+  return d ? (int64_t)d->th * d->tw * d->num_freqs : 0;
+}
+
+int dwm_select_algo(const dwm_desc_t* d, int dtype, int algo) {
+  if (algo == DWM_ALGO_EXACT) return DWM_ALGO_EXACT;
+  const bool tc_ok = dtype == DWM_F32 && tc_gemm_supported(*d);
+  if (algo == DWM_ALGO_TC) return tc_ok ? DWM_ALGO_TC : -1;
+  return (tc_ok && d->c >= 64) ? DWM_ALGO_TC : DWM_ALGO_EXACT;
+}
+
+size_t dwm_workspace_bytes(const dwm_desc_t* d, int dtype, int algo) {
+  if (!d) return 0;
+  const size_t es = dtype == DWM_F64 ? 8 : 4;
+  const int sel = dwm_select_algo(d, dtype, algo);
+  const size_t v = (size_t)d->num_freqs * (size_t)d->tiles * (size_t)d->c * es;
+  size_t u = (size_t)d->num_freqs * (size_t)d->f * (size_t)d->c * es;
+  if (sel == DWM_ALGO_TC) u *= 2;  // hi/lo TF32 split of U
+  const size_t align = 256;
+  return ((v + align - 1) / align) * align + ((u + align - 1) / align) * align;
+}
+
+static int check_common(const dwm_desc_t* d, int dtype) {
+  if (!d) return fail(DWM_EINVAL_SHAPE, "descriptor pointer is NULL");
+  if (dtype != DWM_F32 && dtype != DWM_F64)
+    return fail(DWM_EINVAL_DTYPE, "dtype must be float32 or float64, got code %d", dtype);
+  if (d->num_freqs <= 0 || d->tiles <= 0)
+    return fail(DWM_EINVAL_SHAPE, "descriptor is not initialised (call dwm_desc_init)");
+  return DWM_OK;
+}
+
+int dwm_filter_transform(const dwm_desc_t* d, int dtype, const void* w, void* U, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  return launch_filter_transform(*d, dtype, w, U, (cudaStream_t)stream);
+}
+
+int dwm_input_transform(const dwm_desc_t* d, int dtype, const void* x, void* V, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  return launch_input_transform(*d, dtype, x, V, (cudaStream_t)stream);
+}
+
+int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, const void* U,
+                    void* y, int32_t* flag, void* ws, size_t ws_bytes, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  const int sel = dwm_select_algo(d, dtype, algo);
+  if (sel < 0)
+    return fail(DWM_EUNSUPPORTED,
+                "tcgen05 path needs float32, C %% 32 == 0 and F %% 64 == 0 (got C=%d F=%d)", d->c, d->f);
+  if (sel == DWM_ALGO_TC)
+    return launch_gemm_tc(*d, V, U, y, flag, (cudaStream_t)stream);
+  return launch_gemm_exact(*d, dtype, V, U, y, flag, (cudaStream_t)stream);
+}
+
+int dwm_conv2d_forward(const dwm_desc_t* d, int dtype, int algo, const void* x, const void* w,
+                       void* y, void* ws, size_t ws_bytes, int32_t* flag, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  const int sel = dwm_select_algo(d, dtype, algo);
+  if (sel < 0)
+    return fail(DWM_EUNSUPPORTED,
+                "tcgen05 path needs float32, C %% 32 == 0 and F %% 64 == 0 (got C=%d F=%d)", d->c, d->f);
+  const size_t need = dwm_workspace_bytes(d, dtype, sel);
+  if (!ws || ws_bytes < need)
+    return fail(DWM_EINVAL_SHAPE, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
+  const size_t es = dtype == DWM_F64 ? 8 : 4;
+  const size_t v_bytes = (size_t)d->num_freqs * (size_t)d->tiles * (size_t)d->c * es;
+  char* base = (char*)ws;
+  void* V = base;
+  void* U = base + ((v_bytes + 255) / 256) * 256;
+  cudaStream_t s = (cudaStream_t)stream;
+  int st;
+  if (sel == DWM_ALGO_TC) {
+    if ((st = launch_filter_transform_tf32split(*d, w, U, s))) return st;
+  } else {
+    if ((st = launch_filter_transform(*d, dtype, w, U, s))) return st;
+  }
+  if ((st = launch_input_transform(*d, dtype, x, V, s))) return st;
+  if (sel == DWM_ALGO_TC) return launch_gemm_tc(*d, V, U, y, flag, s);
+  return launch_gemm_exact(*d, dtype, V, U, y, flag, s);
+}
+
+}  // extern "C"

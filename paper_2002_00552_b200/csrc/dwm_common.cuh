@@ -1,0 +1,64 @@
+// dwm_common.cuh -- shared device helpers for the DWM sm_100a kernels.
+//
+// Transform constants F(2,1), F(2,2), F(2,3) (reference transforms.py:129-208
+// with nodes 0, 1, -1, infinity; r == 1 identity, transforms.py:163-167).
+// All entries are 0, +-1 or +-1/2, exactly representable; applied as
+// sequential FMA chains in ascending tap order, which reproduces the
+// reference's BLAS small-K contraction bit for bit.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dwm_b200.h"
+
+namespace dwm {
+
+// [count][row][col]; count index 1..3, unused slots zero.
+// Bt: alpha x alpha, G: alpha x count, At: 2 x alpha.
+static __constant__ float c_bt[4][4][4] = {
+    {},
+    {{1, 0}, {0, 1}},
+    {{1, -1, 0}, {0, 1, 0}, {0, 1, -1}},
+    {{1, 0, -1, 0}, {0, 1, 1, 0}, {0, -1, 1, 0}, {0, 1, 0, -1}},
+};
+static __constant__ float c_g[4][4][3] = {
+    {},
+    {{1}, {1}},
+    {{1, 0}, {1, 1}, {0, 1}},
+    {{1, 0, 0}, {0.5f, 0.5f, 0.5f}, {0.5f, -0.5f, 0.5f}, {0, 0, 1}},
+};
+static __constant__ float c_at[4][2][4] = {
+    {},
+    {{1, 0}, {0, 1}},
+    {{1, 1, 0}, {0, 1, -1}},
+    {{1, 1, 1, 0}, {0, 1, -1, -1}},
+};
+
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// Frequency offset of part p (plan order = row part major, col part minor).
+__host__ __device__ __forceinline__ int part_freq_offset(const dwm_desc_t& d, int p) {
+  int off = 0;
+  for (int q = 0; q < p; ++q) {
+    const int rp = q / d.n_col_parts, cp = q % d.n_col_parts;
+    off += (d.row_parts[rp].count + 1) * (d.col_parts[cp].count + 1);
+  }
+  return off;
+}
+
+#define DWM_CUDA_TRY(expr)                                                  \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) return ::dwm::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+int fail(int status, const char* fmt, ...);
+
+}  // namespace dwm

@@ -1,0 +1,177 @@
+// dwm_gemm_exact.cu -- transform-domain contraction + fused output transform
+// on the CUDA cores, in the reference's exact stage order.
+//
+// Reference rows: M (engines.py:82-89,189), A (engines.py:192-194),
+// Sigma (tensor.py:68-81 at engines.py:254), F (tensor.py:27-30 at engines.py:255).
+//
+// For every (tile, filter) pair a thread owns, and for every part in plan
+// order, frequency by frequency (column frequency b outer, row frequency a
+// inner):
+//   M      = sum_c U[fq][f][c] * V[fq][tile][c]   FMA chain, c ascending
+//   S[i]  += At_r[i][a] * M                       row stage of At.m.A, a ascending
+//   T[i][j] += S[i] * At_c[j][b]                  column stage, b ascending
+//   y      = y + T                                left fold over parts
+// which is the reference's rounding sequence when its BLAS accumulates
+// sequentially (small C).  Only y reaches HBM: the per-part outputs and the
+// per-frequency products stay in registers; non-finite outputs raise a flag.
+#include "dwm_common.cuh"
+#include "dwm_kernels.h"
+
+namespace dwm {
+
+template <typename T, int BM, int BN, int TM, int TN, int KC>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+gemm_exact_kernel(const dwm_desc_t d, const T* __restrict__ V, const T* __restrict__ U,
+                  T* __restrict__ y, int32_t* __restrict__ flag) {
+  constexpr int GM = BM / TM;  // threads along tiles (fast index)
+  constexpr int GN = BN / TN;
+  constexpr int NT = GM * GN;
+  __shared__ T sV[KC][BM + 1];
+  __shared__ T sU[KC][BN + 1];
+
+  const int tid = threadIdx.x;
+  const int tm = tid % GM, tn = tid / GM;
+  const int64_t tile0 = (int64_t)blockIdx.x * BM;
+  const int f0 = blockIdx.y * BN;
+  const int C = d.c, F = d.f;
+  const int64_t tiles = d.tiles;
+
+  T acc[TM][TN][2][2];
+  T Tt[TM][TN][2][2];
+  T S[TM][TN][2];
+
+  int fq_base = 0;
+  for (int p = 0; p < d.n_row_parts * d.n_col_parts; ++p) {
+    const int pr = d.row_parts[p / d.n_col_parts].count;
+    const int pc = d.col_parts[p % d.n_col_parts].count;
+    const int lr = pr + 1, lc = pc + 1;
+    for (int b = 0; b < lc; ++b) {
+      for (int a = 0; a < lr; ++a) {
+        const int fq = fq_base + a * lc + b;
+        const T* Vq = V + (int64_t)fq * tiles * C;
+        const T* Uq = U + (int64_t)fq * F * C;
+        T M[TM][TN];
+        for (int k0 = 0; k0 < C; k0 += KC) {
+          const int kn = min(KC, C - k0);
+          __syncthreads();
+          for (int e = tid; e < BM * KC; e += NT) {
+            const int k = e % KC, t = e / KC;
+            const int64_t tile = tile0 + t;
+            sV[k][t] = (k < kn && tile < tiles) ? Vq[tile * C + k0 + k] : T(0);
+          }
+          for (int e = tid; e < BN * KC; e += NT) {
+            const int k = e % KC, fl = e / KC;
+            sU[k][fl] = (k < kn && f0 + fl < F) ? Uq[(int64_t)(f0 + fl) * C + k0 + k] : T(0);
+          }
+          __syncthreads();
+          for (int k = 0; k < kn; ++k) {
+            T vv[TM], uu[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) vv[i] = sV[k][tm + i * GM];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) uu[j] = sU[k][tn * TN + j];
+            if (k0 + k == 0) {
+#pragma unroll
+              for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) M[i][j] = mul_rn(uu[j], vv[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) M[i][j] = fma_rn(uu[j], vv[i], M[i][j]);
+            }
+          }
+        }
+        // row stage of At.m.A
+        const T ar0 = (T)c_at[pr][0][a], ar1 = (T)c_at[pr][1][a];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            if (a == 0) {
+              S[i][j][0] = mul_rn(ar0, M[i][j]);
+              S[i][j][1] = mul_rn(ar1, M[i][j]);
+            } else {
+              S[i][j][0] = fma_rn(ar0, M[i][j], S[i][j][0]);
+              S[i][j][1] = fma_rn(ar1, M[i][j], S[i][j][1]);
+            }
+          }
+      }
+      // column stage of At.m.A
+      const T ac0 = (T)c_at[pc][0][b], ac1 = (T)c_at[pc][1][b];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            if (b == 0) {
+              Tt[i][j][ii][0] = mul_rn(S[i][j][ii], ac0);
+              Tt[i][j][ii][1] = mul_rn(S[i][j][ii], ac1);
+            } else {
+              Tt[i][j][ii][0] = fma_rn(S[i][j][ii], ac0, Tt[i][j][ii][0]);
+              Tt[i][j][ii][1] = fma_rn(S[i][j][ii], ac1, Tt[i][j][ii][1]);
+            }
+          }
+    }
+    // aggregation in plan order
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+            acc[i][j][ii][jj] = (p == 0) ? Tt[i][j][ii][jj] : add_rn(acc[i][j][ii][jj], Tt[i][j][ii][jj]);
+    fq_base += lr * lc;
+  }
+
+  // epilogue: interleave 2x2 tiles into NCHW and truncate odd extents
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t tile = tile0 + tm + i * GM;
+    if (tile >= tiles) continue;
+    const int tx = (int)(tile % d.tw);
+    const int64_t t2 = tile / d.tw;
+    const int ty = (int)(t2 % d.th);
+    const int n = (int)(t2 / d.th);
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int f = f0 + tn * TN + j;
+      if (f >= F) continue;
+      T* yf = y + ((int64_t)n * F + f) * d.oh * d.ow;
+#pragma unroll
+      for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int oy = 2 * ty + ii, ox = 2 * tx + jj;
+          if (oy < d.oh && ox < d.ow) {
+            const T v = acc[i][j][ii][jj];
+            bad |= !isfinite(v);
+            yf[(int64_t)oy * d.ow + ox] = v;
+          }
+        }
+    }
+  }
+  if (bad && flag) *flag = 1;
+}
+
+int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void* U, void* y,
+                      int32_t* flag, cudaStream_t s) {
+  constexpr int BM = 64, BN = 32, TM = 2, TN = 4, KC = 16;
+  const dim3 grid((unsigned)((d.tiles + BM - 1) / BM), (unsigned)((d.f + BN - 1) / BN));
+  const int threads = (BM / TM) * (BN / TN);
+  if (dtype == DWM_F64)
+    gemm_exact_kernel<double, BM, BN, TM, TN, KC><<<grid, threads, 0, s>>>(
+        d, (const double*)V, (const double*)U, (double*)y, flag);
+  else
+    gemm_exact_kernel<float, BM, BN, TM, TN, KC><<<grid, threads, 0, s>>>(
+        d, (const float*)V, (const float*)U, (float*)y, flag);
+  DWM_CUDA_TRY(cudaGetLastError());
+  return DWM_OK;
+}
+
+}  // namespace dwm

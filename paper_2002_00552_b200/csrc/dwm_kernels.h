@@ -1,0 +1,19 @@
+// dwm_kernels.h -- internal launcher declarations (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/dwm_b200.h"
+
+namespace dwm {
+
+int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s);
+// U_hi | U_lo (each [freq][F][C] fp32, TF32-valued, RN split) for the tcgen05 path.
+int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s);
+int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s);
+int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void* U, void* y,
+                      int32_t* flag, cudaStream_t s);
+bool tc_gemm_supported(const dwm_desc_t& d);
+int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag,
+                   cudaStream_t s);
+
+}  // namespace dwm

@@ -1,0 +1,214 @@
+// dwm_transforms.cu -- filter transform (U = G g Gt) and input-tile transform
+// (V = Bt d B with the polyphase stride gather) for every decomposition part.
+//
+// Reference rows: W (kernel sub-block gather, engines.py:246-248),
+// U (engines.py:187), G (strided slice + even zero-extension + windows,
+// tensor.py:45-65, engines.py:104-120), V (engines.py:186).
+//
+// Both transforms apply the row stage then the column stage as sequential
+// FMA chains in ascending tap order, so U and V are bit-identical to the
+// reference's binary32/binary64 values (the coefficients are 0, +-1, +-1/2).
+#include "dwm_common.cuh"
+#include "dwm_kernels.h"
+
+namespace dwm {
+
+// ---------------------------------------------------------------------------
+// Filter transform: one thread per (f, c); U[fq][f][c].
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void part_filter_transform(const dwm_desc_t& d, const T* __restrict__ wfc,
+                                                      int rp, int cp, T out[4][4]) {
+  const dwm_axis_part_t R = d.row_parts[rp], Cc = d.col_parts[cp];
+  const int pr = R.count, pc = Cc.count;
+  T g[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      g[i][j] = (i < pr && j < pc) ? wfc[(R.origin + R.step * i) * d.r_w + Cc.origin + Cc.step * j] : T(0);
+  // row stage: t[u][j] = sum_i G_r[u][i] * g[i][j]
+  T t[4][3];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      T acc = mul_rn((T)c_g[pr][u][0], g[0][j]);
+#pragma unroll
+      for (int i = 1; i < 3; ++i)
+        if (i < pr) acc = fma_rn((T)c_g[pr][u][i], g[i][j], acc);
+      t[u][j] = acc;
+    }
+  // column stage: U[u][v] = sum_j t[u][j] * G_c[v][j]
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      T acc = mul_rn(t[u][0], (T)c_g[pc][v][0]);
+#pragma unroll
+      for (int j = 1; j < 3; ++j)
+        if (j < pc) acc = fma_rn(t[u][j], (T)c_g[pc][v][j], acc);
+      out[u][v] = acc;
+    }
+}
+
+template <typename T>
+__global__ void filter_transform_kernel(const dwm_desc_t d, const T* __restrict__ w, T* __restrict__ U) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t fc = (int64_t)d.f * d.c;
+  if (idx >= fc) return;
+  const T* wfc = w + idx * d.r_h * d.r_w;  // idx = f*C + c
+  int fq = 0;
+  for (int rp = 0; rp < d.n_row_parts; ++rp)
+    for (int cp = 0; cp < d.n_col_parts; ++cp) {
+      T u[4][4];
+      part_filter_transform(d, wfc, rp, cp, u);
+      const int lr = d.row_parts[rp].count + 1, lc = d.col_parts[cp].count + 1;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (a < lr && b < lc) U[(int64_t)(fq + a * lc + b) * fc + idx] = u[a][b];
+      fq += lr * lc;
+    }
+}
+
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// U_hi = tf32(U), U_lo = tf32(U - U_hi), two [freq][F][C] planes.
+__global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const float* __restrict__ w,
+                                                  float* __restrict__ U) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t fc = (int64_t)d.f * d.c;
+  if (idx >= fc) return;
+  const int64_t plane = (int64_t)d.num_freqs * fc;
+  const float* wfc = w + idx * d.r_h * d.r_w;
+  int fq = 0;
+  for (int rp = 0; rp < d.n_row_parts; ++rp)
+    for (int cp = 0; cp < d.n_col_parts; ++cp) {
+      float u[4][4];
+      part_filter_transform(d, wfc, rp, cp, u);
+      const int lr = d.row_parts[rp].count + 1, lc = d.col_parts[cp].count + 1;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (a < lr && b < lc) {
+            const float hi = tf32_rn(u[a][b]);
+            const float lo = tf32_rn(u[a][b] - hi);
+            const int64_t o = (int64_t)(fq + a * lc + b) * fc + idx;
+            U[o] = hi;
+            U[plane + o] = lo;
+          }
+      fq += lr * lc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Input transform: one thread per (tile, c), c fastest; V[fq][tile][c].
+// Window sample (i, j) of part (rp, cp) for tile (ty, tx) is padded-input
+// row a_r + s_h*(2ty+i), col a_c + s_w*(2tx+j)  (decompose.py:117-133), zero
+// when it falls in the padding or past the part's strided slice
+// (k >= OUT-1+count: the reference's even-extension zeros, engines.py:109-115).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= d.tiles * d.c) return;
+  const int c = (int)(idx % d.c);
+  const int64_t tile = idx / d.c;
+  const int tx = (int)(tile % d.tw);
+  const int64_t t2 = tile / d.tw;
+  const int ty = (int)(t2 % d.th);
+  const int n = (int)(t2 / d.th);
+  const T* xc = x + ((int64_t)n * d.c + c) * d.h * d.w;
+  const int64_t tc_stride = d.tiles * d.c;
+  int fq = 0;
+  for (int rp = 0; rp < d.n_row_parts; ++rp) {
+    const dwm_axis_part_t R = d.row_parts[rp];
+    const int pr = R.count, lr = pr + 1;
+    int rows[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = 2 * ty + i;
+      const int row = R.origin + d.s_h * k - d.pad_top;
+      rows[i] = (i < lr && k < d.oh - 1 + pr && row >= 0 && row < d.h) ? row : -1;
+    }
+    for (int cp = 0; cp < d.n_col_parts; ++cp) {
+      const dwm_axis_part_t Cc = d.col_parts[cp];
+      const int pc = Cc.count, lc = pc + 1;
+      int cols[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = 2 * tx + j;
+        const int col = Cc.origin + d.s_w * k - d.pad_left;
+        cols[j] = (j < lc && k < d.ow - 1 + pc && col >= 0 && col < d.w) ? col : -1;
+      }
+      T win[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? __ldg(xc + (int64_t)rows[i] * d.w + cols[j]) : T(0);
+      // row stage t[a][j] = sum_i Bt_r[a][i] win[i][j]; column stage v[a][b] = sum_j t[a][j] Bt_c[b][j]
+      T t[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          T acc = mul_rn((T)c_bt[pr][a][0], win[0][j]);
+#pragma unroll
+          for (int i = 1; i < 4; ++i)
+            if (i < lr) acc = fma_rn((T)c_bt[pr][a][i], win[i][j], acc);
+          t[a][j] = acc;
+        }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (a < lr && b < lc) {
+            T acc = mul_rn(t[a][0], (T)c_bt[pc][b][0]);
+#pragma unroll
+            for (int j = 1; j < 4; ++j)
+              if (j < lc) acc = fma_rn(t[a][j], (T)c_bt[pc][b][j], acc);
+            V[(int64_t)(fq + a * lc + b) * tc_stride + idx] = acc;
+          }
+      fq += lr * lc;
+    }
+  }
+}
+
+static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s) {
+  const int64_t n = (int64_t)d.f * d.c;
+  if (dtype == DWM_F64)
+    filter_transform_kernel<double><<<grid_for(n, 128), 128, 0, s>>>(d, (const double*)w, (double*)U);
+  else
+    filter_transform_kernel<float><<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, (float*)U);
+  DWM_CUDA_TRY(cudaGetLastError());
+  return DWM_OK;
+}
+
+int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s) {
+  const int64_t n = (int64_t)d.f * d.c;
+  filter_transform_tf32split_kernel<<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, (float*)U);
+  DWM_CUDA_TRY(cudaGetLastError());
+  return DWM_OK;
+}
+
+int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s) {
+  const int64_t n = d.tiles * d.c;
+  if (dtype == DWM_F64)
+    input_transform_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(d, (const double*)x, (double*)V);
+  else
+    input_transform_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(d, (const float*)x, (float*)V);
+  DWM_CUDA_TRY(cudaGetLastError());
+  return DWM_OK;
+}
+
+}  // namespace dwm

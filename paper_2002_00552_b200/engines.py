@@ -1,0 +1,213 @@
+"""Drop-in DWM forward entry point on B200.
+
+``dwm_conv2d(data, weights, spec, plan=None, precision=None, counter=None)``
+keeps the reference signature, argument meaning, error types and messages
+(reference ``pkg/src/dwmconv/engines.py:219-255``) and runs the whole
+forward on the GPU through the C ABI (``include/dwm_b200.h``):
+
+  filter transform  (U = G g Gt per part)           dwm_transforms.cu
+  input transform   (V = Bt d B, polyphase gather)   dwm_transforms.cu
+  transform-domain contraction + fused At.m.A,
+  plan-order part sum, tile interleave, finiteness   dwm_gemm_exact.cu / dwm_gemm_tc.cu
+
+Inputs may be NumPy arrays (copied to the GPU, result copied back as NumPy,
+exactly like the reference's return type) or torch tensors (CUDA tensors stay
+on the device; CPU tensors are staged through the GPU and returned on the CPU).
+binary32 and binary64 are supported; the exact-rational object dtype of the
+reference's test mode is not (TypeError).  There is no CPU fallback: without
+the native library or a CUDA device every call raises.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .convspec import ConvSpec
+from .decompose import DecompositionPlan, plan_decomposition
+from .transforms import precision_dtype
+
+FLOAT_DTYPES = (np.dtype(np.float32), np.dtype(np.float64))
+
+
+@dataclass(frozen=True)
+class ConvOutput:
+    """Result plus the elementwise-product count (reference engines.py:32-41)."""
+
+    y: object
+    flops: object = None
+
+
+class FlopCounter:
+    """Mutable tally of transform-domain products (reference engines.py:44-48)."""
+
+    def __init__(self):
+        self.elementwise = 0
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _require_tensor4(x, name: str):
+    """reference tensor.py:16-24 (torch tensors accepted as well)."""
+    if _is_torch(x):
+        if x.dim() != 4:
+            raise ValueError(f"{name} must have 4 axes (N,C,H,W), got shape {tuple(x.shape)}")
+        torch = _torch()
+        if x.dtype not in (torch.float32, torch.float64):
+            raise TypeError(f"{name} must be float32 or float64, got {x.dtype}")
+        return x
+    if not isinstance(x, np.ndarray):
+        raise TypeError(f"{name} must be a numpy array, got {type(x).__name__}")
+    if x.ndim != 4:
+        raise ValueError(f"{name} must have 4 axes (N,C,H,W), got shape {x.shape}")
+    if x.dtype == np.dtype(object):
+        raise TypeError(f"{name}: the exact-rational object dtype runs only in the reference's "
+                        "CPU test mode; the B200 path computes in binary32/binary64")
+    if x.dtype not in FLOAT_DTYPES:
+        raise TypeError(f"{name} must be float32 or float64, got {x.dtype}")
+    return x
+
+
+def _np_dtype(x) -> np.dtype:
+    if _is_torch(x):
+        return np.dtype(np.float64) if x.dtype == _torch().float64 else np.dtype(np.float32)
+    return x.dtype
+
+
+def _check_pair(data, weights):
+    """reference engines.py:63-68"""
+    _require_tensor4(data, "data")
+    _require_tensor4(weights, "weights")
+    if data.shape[1] != weights.shape[1]:
+        raise ValueError(
+            f"channel mismatch: data has {data.shape[1]}, weights have {weights.shape[1]}")
+
+
+_WORKSPACE = {}
+
+
+def _workspace(device, nbytes: int):
+    """Grow-only per-device scratch for V and U (stream-ordered reuse)."""
+    torch = _torch()
+    buf = _WORKSPACE.get(device)
+    if buf is None or buf.numel() < nbytes:
+        _WORKSPACE.pop(device, None)
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WORKSPACE[device] = buf
+    return buf
+
+
+def _check_plan_matches(plan: DecompositionPlan, desc) -> None:
+    rows = [(p.origin, p.step, p.count) for p in plan.row_parts]
+    cols = [(p.origin, p.step, p.count) for p in plan.col_parts]
+    if rows != desc.axis("row") or cols != desc.axis("col"):
+        raise AssertionError(f"native planner disagrees with the host plan: {rows}/{cols} vs "
+                             f"{desc.axis('row')}/{desc.axis('col')}")
+
+
+def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
+               precision=None, counter: FlopCounter = None, *, algo: str = "auto",
+               check_finite: bool = True, out=None, stream=None):
+    """Decomposed Winograd convolution for any kernel size and stride, on B200.
+
+    Same contract as the reference (engines.py:219-255): pads once, runs every
+    plan part as a stride-1 F(2, <=3) Winograd convolution, sums parts in plan
+    order, raises FloatingPointError on non-finite output.  Keyword-only
+    extras: ``algo`` ("auto" | "exact" | "tc"), ``check_finite`` (skip the
+    device->host flag read for fully asynchronous use), ``out`` (preallocated
+    CUDA output tensor) and ``stream`` (torch.cuda.Stream; default current).
+    """
+    _check_pair(data, weights)
+    if tuple(weights.shape[2:]) != spec.kernel:
+        raise ValueError(f"weights taps {tuple(weights.shape[2:])} do not match kernel {spec.kernel}")
+    if plan is None:
+        plan = plan_decomposition(spec)
+    elif plan.spec != spec:
+        raise ValueError("plan was built for a different ConvSpec")
+    dt = _np_dtype(data) if precision is None else precision_dtype(precision)
+    n, c, h, w = (int(s) for s in data.shape)
+    f = int(weights.shape[0])
+    spec.out_dims(h, w)  # geometry errors with the reference's message
+
+    torch = _torch()
+    lib = _native.load()
+    if not torch.cuda.is_available():
+        raise _native.NativeError("dwm_conv2d needs a CUDA device (B200); there is no CPU fallback")
+    tdt = torch.float64 if dt == np.dtype(np.float64) else torch.float32
+    code = _native.DWM_F64 if tdt == torch.float64 else _native.DWM_F32
+
+    desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+    _check_plan_matches(plan, desc)
+
+    from_numpy = not _is_torch(data)
+    if from_numpy:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x_d = torch.from_numpy(np.ascontiguousarray(data)).to(dev, dtype=tdt)
+    else:
+        dev = data.device if data.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        x_d = data.to(dev, dtype=tdt, non_blocking=True).contiguous()
+    w_d = (torch.from_numpy(np.ascontiguousarray(weights)) if not _is_torch(weights)
+           else weights).to(dev, dtype=tdt).contiguous()
+
+    oh, ow = desc.oh, desc.ow
+    if out is not None:
+        if tuple(out.shape) != (n, f, oh, ow) or out.dtype != tdt or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous {(n, f, oh, ow)} {tdt} tensor")
+        y_d = out if out.is_cuda else torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
+    else:
+        y_d = torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
+    algo_code = _native.ALGOS[algo]
+    ws_bytes = lib.dwm_workspace_bytes(desc, code, algo_code)
+    with torch.cuda.device(dev):
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        ws = _workspace(dev, ws_bytes)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+        st = lib.dwm_conv2d_forward(desc, code, algo_code, x_d.data_ptr(), w_d.data_ptr(),
+                                    y_d.data_ptr(), ws.data_ptr(), ws_bytes,
+                                    flag.data_ptr() if flag is not None else None,
+                                    s.cuda_stream)
+        _native.check(st, "dwm_conv2d_forward")
+        if counter is not None:
+            counter.elementwise += int(lib.dwm_elementwise_count(desc))
+        if check_finite and int(flag.item()) != 0:
+            raise FloatingPointError("dwm_conv2d produced non-finite values")
+    if out is not None and not out.is_cuda:
+        out.copy_(y_d)
+        return out
+    if from_numpy:
+        return y_d.cpu().numpy()
+    if not data.is_cuda:
+        return y_d.cpu()
+    return y_d
+
+
+def convolve(data, weights, spec: ConvSpec, algo: str = "dwm", precision=None,
+             plan: DecompositionPlan = None) -> ConvOutput:
+    """Instrumented run by name (reference engines.py:402-421); only "dwm"
+    is on the B200 path -- "direct"/"winograd" are the reference's CPU
+    baselines and are out of scope here."""
+    if algo != "dwm":
+        raise ValueError(f"unknown algorithm {algo!r} for the B200 path; only 'dwm' is implemented "
+                         "(direct and classic Winograd are the reference's CPU baselines)")
+    counter = FlopCounter()
+    y = dwm_conv2d(data, weights, spec, plan=plan, precision=precision, counter=counter)
+    return ConvOutput(y=y, flops=counter.elementwise)
+
+
+def flops_dwm(plan: DecompositionPlan, out) -> int:
+    """tiles * sum over parts of alpha_r * alpha_c (reference flops.py:107-119;
+    the transform terms are zero because F(2,<=3) is shift-free)."""
+    oh, ow = out
+    tiles = -(-oh // 2) * -(-ow // 2)
+    return tiles * plan.num_frequencies

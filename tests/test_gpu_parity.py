@@ -1,0 +1,151 @@
+"""GPU parity: the CUDA path (through the C ABI / the drop-in entry point)
+against the oracle and the reference's golden outputs.
+
+Tolerances (written here):
+  * U and V stage outputs: bit-identical (np.array_equal) to the reference's
+    per-part transforms, binary32 and binary64.
+  * "exact" engine, binary64: max |gpu - reference dwm64| <= 1e-12 and
+    <= 1e-10 vs the FP64 direct conv (reference acceptance, test_acceptance.py:65-78).
+  * "exact" engine, binary32: bit-identical to the reference for C_in <= 4
+    (where the reference's BLAS sums sequentially); otherwise
+    max |gpu - ref32| <= 4e-5 * max|y|.
+  * every engine, BASELINE workloads (one image, seed 1, bench.py:103-109 recipe):
+    MSE vs FP64 direct <= 1e-7 (bench.py:179) and <= MSE_TOL x the
+    reference DWM32 MSE (north star: "at or below the reference's").
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle.dwm_oracle import (direct_conv2d_f64, draw, dwm_conv2d_oracle, filter_transform_oracle,
+                               input_transform_oracle, mse)
+from paper_2002_00552_b200 import (ConvSpec, FlopCounter, dwm_conv2d, flops_dwm,
+                                   plan_decomposition)
+from paper_2002_00552_b200 import _native
+from paper_2002_00552_b200.configs import WORKLOADS
+
+pytestmark = pytest.mark.gpu
+
+CASES = json.loads((GOLDEN / "cases.json").read_text())
+ARR = np.load(GOLDEN / "small_cases.npz")
+BASE = json.loads((GOLDEN / "baseline_samples.json").read_text())
+MSE_TOL = {"exact": 1.02, "tc": 1.0}
+
+
+def _spec(case):
+    return ConvSpec(kernel=tuple(case["kernel"]), stride=tuple(case["stride"]), pad=tuple(case["pad"]))
+
+
+def _stage(torch, fn, desc, dtype, src, out_shape, dev):
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    code = _native.DWM_F64 if dtype == np.float64 else _native.DWM_F32
+    s = torch.from_numpy(np.ascontiguousarray(src)).to(dev, dtype=tdt)
+    o = torch.full(out_shape, float("nan"), dtype=tdt, device=dev)
+    _native.check(fn(desc, code, s.data_ptr(), o.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return o.cpu().numpy()
+
+
+@pytest.mark.parametrize("case", CASES[::3], ids=[c["name"] for c in CASES[::3]])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_filter_and_input_transforms_bit_exact(cuda, case, dtype):
+    import torch
+    d, g = ARR[f"{case['name']}/data"], ARR[f"{case['name']}/weights"]
+    spec = _spec(case)
+    n, c, h, w = d.shape
+    f = g.shape[0]
+    desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+    lib = _native.load()
+    u_ref = filter_transform_oracle(g, spec, dtype)
+    u = _stage(torch, lib.dwm_filter_transform, desc, dtype, g.astype(dtype), u_ref.shape, cuda)
+    assert np.array_equal(u, u_ref)
+    v_ref = input_transform_oracle(d, spec, dtype)
+    v = _stage(torch, lib.dwm_input_transform, desc, dtype, d.astype(dtype), v_ref.shape, cuda)
+    assert np.array_equal(v, v_ref)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_exact_engine_matches_reference_golden(cuda, case):
+    d, g = ARR[f"{case['name']}/data"], ARR[f"{case['name']}/weights"]
+    spec = _spec(case)
+    y64 = dwm_conv2d(d, g, spec, algo="exact")                      # float64 inputs -> binary64
+    assert y64.dtype == np.float64
+    assert np.max(np.abs(y64 - ARR[f"{case['name']}/dwm64"])) <= 1e-12
+    assert np.max(np.abs(y64 - ARR[f"{case['name']}/direct64"])) <= 1e-10
+    y32 = dwm_conv2d(d, g, spec, precision="binary32", algo="exact")
+    ref32 = ARR[f"{case['name']}/dwm32"]
+    assert y32.dtype == np.float32 and y32.shape == ref32.shape
+    if d.shape[1] <= 4:
+        assert np.array_equal(y32, ref32), np.max(np.abs(y32 - ref32))
+    else:
+        assert np.max(np.abs(y32 - ref32)) <= 4e-5 * max(1.0, np.max(np.abs(ref32)))
+
+
+def _run_workload(name, algo, cuda):
+    wl = WORKLOADS[name]
+    d, g = draw(1, (wl.kernel,) * 2, (wl.stride,) * 2, wl.hw, wl.c_in, wl.c_out, 1)
+    spec = wl.spec()
+    y = dwm_conv2d(d.astype(np.float32), g.astype(np.float32), spec, algo=algo)
+    return d, g, spec, y
+
+
+@pytest.mark.parametrize("name", list(WORKLOADS))
+def test_baseline_workload_accuracy_exact(cuda, name):
+    d, g, spec, y = _run_workload(name, "exact", cuda)
+    y64 = direct_conv2d_f64(d, g, spec)
+    gold = BASE[name]
+    m = mse(y, y64)
+    assert m <= 1e-7
+    assert m <= MSE_TOL["exact"] * gold["dwm32_mse"], (m, gold["dwm32_mse"])
+    idx = tuple(np.array(gold["index"]).T)
+    np.testing.assert_allclose(y[idx], gold["dwm32"], rtol=0, atol=1e-3)
+    np.testing.assert_allclose(y[idx], gold["direct64"], rtol=0, atol=5e-3)
+
+
+def test_torch_tensor_io_and_counter(cuda):
+    import torch
+    spec = ConvSpec(kernel=(5, 5), stride=(2, 2), pad=(2, 2, 2, 2))
+    d = torch.randn(2, 3, 15, 15, device=cuda)
+    g = torch.randn(4, 3, 5, 5, device=cuda)
+    counter = FlopCounter()
+    y = dwm_conv2d(d, g, spec, counter=counter)
+    assert y.is_cuda and y.shape == (2, 4, 8, 8) and y.dtype == torch.float32
+    assert counter.elementwise == flops_dwm(plan_decomposition(spec), (8, 8))
+    want = dwm_conv2d_oracle(d.cpu().numpy(), g.cpu().numpy(), spec)
+    np.testing.assert_allclose(y.cpu().numpy(), want, rtol=0, atol=1e-4)
+    y_cpu = dwm_conv2d(d.cpu(), g.cpu(), spec)
+    assert not y_cpu.is_cuda and torch.equal(y_cpu, y.cpu())
+
+
+def test_nonfinite_raises(cuda):                  # test_engines_forward.py:216-220
+    d = np.full((1, 1, 8, 8), 1e30, np.float32)
+    g = np.full((1, 1, 3, 3), 1e30, np.float32)
+    with pytest.raises(FloatingPointError, match="non-finite"):
+        dwm_conv2d(d, g, ConvSpec(kernel=(3, 3)))
+
+
+def test_deterministic_run_to_run(cuda):          # test_acceptance.py:187-229
+    wl = WORKLOADS["cfg5-5x5s2"]
+    d, g = draw(2, (5, 5), (2, 2), 56, 128, 256, 2)
+    a = dwm_conv2d(d.astype(np.float32), g.astype(np.float32), wl.spec())
+    b = dwm_conv2d(d.astype(np.float32), g.astype(np.float32), wl.spec())
+    assert a.tobytes() == b.tobytes()
+
+
+def test_full_batch_shard_invariance(cuda):
+    """Size-independent property at BASELINE's full batch: every image of the
+    256-image cfg2 batch equals that image convolved alone (images are
+    independent), bit for bit -- what batch sharding across GPUs relies on."""
+    import torch
+    wl = WORKLOADS["cfg2-resnet50-stem"]
+    gen = torch.Generator(device=cuda).manual_seed(7)
+    x = torch.randn(wl.batch, wl.c_in, wl.hw, wl.hw, device=cuda, generator=gen)
+    w = torch.randn(wl.c_out, wl.c_in, wl.kernel, wl.kernel, device=cuda, generator=gen)
+    y = dwm_conv2d(x, w, wl.spec())
+    for i in (0, 77, 255):
+        yi = dwm_conv2d(x[i:i + 1].contiguous(), w, wl.spec())
+        assert torch.equal(yi[0], y[i])
+    assert torch.isfinite(y).all()
