@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
-    ap.add_argument("--algo", default="auto", choices=["auto", "exact", "tc"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "exact", "tc", "small_c"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=None, help="override per-GPU batch (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -231,7 +231,7 @@ def main():
     desc = _native.make_desc(batch, wl.c_in, wl.hw, wl.hw, wl.c_out, spec.kernel, spec.stride, spec.pad)
     algo = _native.ALGOS[args.algo]
     sel = lib.dwm_select_algo(desc, _native.DWM_F32, algo)
-    algo_name = {1: "exact", 2: "tc"}.get(sel, "?")
+    algo_name = _native.ALGO_NAMES.get(sel, "?")
     ws_bytes = lib.dwm_workspace_bytes(desc, _native.DWM_F32, algo)
 
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -244,7 +244,7 @@ def main():
     sptr = stream.cuda_stream
 
     x_bytes, w_bytes, y_bytes = x.numel() * 4, w.numel() * 4, y.numel() * 4
-    v_bytes = desc.num_freqs * desc.tiles * wl.c_in * 4
+    v_bytes = 0 if algo_name == "small_c" else desc.num_freqs * desc.tiles * wl.c_in * 4
     u_bytes = desc.num_freqs * wl.c_out * wl.c_in * 4 * (2 if algo_name == "tc" else 1)
     working_set = x_bytes + y_bytes + v_bytes
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if working_set < 4 * L2_BYTES else None
@@ -285,7 +285,7 @@ def main():
         total_ms = float(t.item())
     images = batch * world * args.steps
     value = images / (total_ms / 1e3)
-    launches_per_step = 3
+    launches_per_step = 2 if algo_name == "small_c" else 3
 
     # ---- per-stage kernel times (same stream, CUDA events, after the timed region)
     stage_ms = stage_times(lib, desc, algo, algo_name, x, w, y, ws, flag, sptr, stream, flush, reps=max(3, args.steps))
@@ -335,10 +335,11 @@ def main():
 
 
 def stage_times(lib, desc, algo, algo_name, x, w, y, ws, flag, sptr, stream, flush, reps):
+    """Median CUDA-event time of each kernel the forward launches, run alone."""
     import torch
     from paper_2002_00552_b200 import _native
     ws_ptr = ws.data_ptr()
-    v_bytes = desc.num_freqs * desc.tiles * desc.c * 4
+    v_bytes = 0 if algo_name == "small_c" else desc.num_freqs * desc.tiles * desc.c * 4
     V = ws_ptr
     U = ws_ptr + ((v_bytes + 255) // 256) * 256
     F32 = _native.DWM_F32
@@ -353,13 +354,19 @@ def stage_times(lib, desc, algo, algo_name, x, w, y, ws, flag, sptr, stream, flu
         _native.check(lib.dwm_gemm_output(desc, F32, algo, V, U, y.data_ptr(), flag.data_ptr(),
                                           None, 0, sptr))
 
-    out = {}
-    # run the full forward once so V/U hold the right (algo-specific) contents
+    def small_c():
+        _native.check(lib.dwm_conv2d_small_c(desc, x.data_ptr(), U, y.data_ptr(), flag.data_ptr(), sptr))
+
+    # one full forward so V/U hold the engine's (layout-specific) contents
     _native.check(lib.dwm_conv2d_forward(desc, F32, algo, x.data_ptr(), w.data_ptr(), y.data_ptr(),
                                          ws_ptr, ws.numel(), flag.data_ptr(), sptr))
-    names = [("input_transform", inp), ("gemm_output", gemm)]
-    if algo_name != "tc":
-        names.insert(0, ("filter_transform", filt))
+    if algo_name == "small_c":
+        names = [("filter_transform", filt), ("conv2d_small_c", small_c)]
+    elif algo_name == "tc":
+        names = [("input_transform", inp), ("gemm_output", gemm)]
+    else:
+        names = [("filter_transform", filt), ("input_transform", inp), ("gemm_output", gemm)]
+    out = {}
     for name, fn in names:
         ms = []
         for _ in range(reps):
@@ -383,11 +390,12 @@ def make_roofline(stage_ms, desc, wl, batch, algo_name, peaks, x_bytes, w_bytes,
         "filter_transform": w_bytes + u_bytes,
         "input_transform": x_bytes + v_bytes,
         "gemm_output": v_bytes + u_bytes + y_bytes,
+        "conv2d_small_c": x_bytes + u_bytes + y_bytes,
     }
     for name, ms in stage_ms.items():
         k = {"name": name, "ms": ms, "alg_bytes": alg_bytes[name],
              "achieved_gbs": alg_bytes[name] / (ms * 1e-3) / 1e9}
-        if name == "gemm_output":
+        if name in ("gemm_output", "conv2d_small_c"):
             k["dwm_gemm_flops"] = gemm_flops
             k["achieved_tflops"] = gemm_flops / (ms * 1e-3) / 1e12
         kernels.append(k)

@@ -49,15 +49,20 @@ typedef enum dwm_status {
 typedef enum dwm_dtype { DWM_F32 = 0, DWM_F64 = 1 } dwm_dtype;
 
 /* Transform-domain contraction engine.
- *   EXACT: CUDA-core FMA chains in the reference's stage order (channel-
- *          ascending GEMM, At.m.A row then column stage, plan-order part
- *          sum).  Bit-identical to the reference where its BLAS accumulates
- *          sequentially (small C); f32 and f64.
- *   TC:    tcgen05/TMEM 3xTF32 GEMM with the output transform, part sum and
- *          tile interleave fused in the epilogue (f32 only, C % 32 == 0,
- *          F % 64 == 0).
- *   AUTO:  TC when eligible and C is large enough to use it, else EXACT. */
-typedef enum dwm_algo { DWM_ALGO_AUTO = 0, DWM_ALGO_EXACT = 1, DWM_ALGO_TC = 2 } dwm_algo;
+ *   EXACT:   CUDA-core FMA chains in the reference's stage order (channel-
+ *            ascending GEMM, At.m.A row then column stage, plan-order part
+ *            sum) over a V workspace.  Bit-identical to the reference where
+ *            its BLAS accumulates sequentially (small C); f32 and f64.
+ *   TC:      tcgen05/TMEM 3xTF32 GEMM with the output transform, part sum and
+ *            tile interleave fused in the epilogue (f32 only, C % 32 == 0,
+ *            F % 64 == 0).
+ *   SMALL_C: one fused kernel (input transform computed in shared memory,
+ *            same arithmetic as EXACT, no V workspace); f32, C_in <= 4.
+ *   AUTO:    SMALL_C for C_in <= 4, TC when eligible and C_in >= 64, else
+ *            EXACT.  dwm_select_algo() reports the resolved engine. */
+typedef enum dwm_algo {
+  DWM_ALGO_AUTO = 0, DWM_ALGO_EXACT = 1, DWM_ALGO_TC = 2, DWM_ALGO_SMALL_C = 3
+} dwm_algo;
 
 /* One strided run of kernel taps along an axis: origin + step*i, i < count
  * (reference AxisPart, decompose.py:25-35). */
@@ -110,6 +115,11 @@ int dwm_input_transform(const dwm_desc_t* desc, int dtype, const void* x,
 int dwm_gemm_output(const dwm_desc_t* desc, int dtype, int algo, const void* V,
                     const void* U, void* y, int32_t* nonfinite_flag,
                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Fused small-C forward (DWM_ALGO_SMALL_C) from the filter-transform
+ * output U ([num_freqs][F][C], f32): gathers and transforms x on chip. */
+int dwm_conv2d_small_c(const dwm_desc_t* desc, const void* x, const void* U,
+                       void* y, int32_t* nonfinite_flag, void* stream);
 
 /* Whole forward: y[N,F,OH,OW] = dwm_conv2d(x[N,C,H,W], w[F,C,r_h,r_w]).
  * nonfinite_flag (device int32, may be NULL) is set to 1 when any output

@@ -106,21 +106,35 @@ int64_t dwm_elementwise_count(const dwm_desc_t* d) {
 }
 
 int dwm_select_algo(const dwm_desc_t* d, int dtype, int algo) {
-  if (algo == DWM_ALGO_EXACT) return DWM_ALGO_EXACT;
+  if (!d) return -1;
   const bool tc_ok = dtype == DWM_F32 && tc_gemm_supported(*d);
-  if (algo == DWM_ALGO_TC) return tc_ok ? DWM_ALGO_TC : -1;
-  return (tc_ok && d->c >= 64) ? DWM_ALGO_TC : DWM_ALGO_EXACT;
+  const bool sc_ok = dtype == DWM_F32 && small_c_supported(*d);
+  switch (algo) {
+    case DWM_ALGO_EXACT: return DWM_ALGO_EXACT;
+    case DWM_ALGO_TC: return tc_ok ? DWM_ALGO_TC : -1;
+    case DWM_ALGO_SMALL_C: return sc_ok ? DWM_ALGO_SMALL_C : -1;
+    case DWM_ALGO_AUTO:
+      if (sc_ok) return DWM_ALGO_SMALL_C;
+      if (tc_ok && d->c >= 64) return DWM_ALGO_TC;
+      return DWM_ALGO_EXACT;
+    default: return -1;
+  }
+}
+
+static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static size_t v_bytes_of(const dwm_desc_t* d, size_t es) {
+  return (size_t)d->num_freqs * (size_t)d->tiles * (size_t)d->c * es;
 }
 
 size_t dwm_workspace_bytes(const dwm_desc_t* d, int dtype, int algo) {
   if (!d) return 0;
   const size_t es = dtype == DWM_F64 ? 8 : 4;
   const int sel = dwm_select_algo(d, dtype, algo);
-  const size_t v = (size_t)d->num_freqs * (size_t)d->tiles * (size_t)d->c * es;
   size_t u = (size_t)d->num_freqs * (size_t)d->f * (size_t)d->c * es;
   if (sel == DWM_ALGO_TC) u *= 2;  // hi/lo TF32 split of U
-  const size_t align = 256;
-  return ((v + align - 1) / align) * align + ((u + align - 1) / align) * align;
+  const size_t v = sel == DWM_ALGO_SMALL_C ? 0 : v_bytes_of(d, es);
+  return round_up(v, 256) + round_up(u, 256);
 }
 
 static int check_common(const dwm_desc_t* d, int dtype) {
@@ -142,33 +156,42 @@ int dwm_input_transform(const dwm_desc_t* d, int dtype, const void* x, void* V, 
   return launch_input_transform(*d, dtype, x, V, (cudaStream_t)stream);
 }
 
+static int bad_algo(const dwm_desc_t* d, int algo) {
+  return fail(DWM_EUNSUPPORTED,
+              "engine %d not available for this geometry/dtype (tcgen05: float32, C %% 32 == 0, "
+              "F %% 64 == 0; small-C: float32, C <= 4; got C=%d F=%d)", algo, d->c, d->f);
+}
+
 int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, const void* U,
                     void* y, int32_t* flag, void* ws, size_t ws_bytes, void* stream) {
   if (int st = check_common(d, dtype)) return st;
-  const int sel = dwm_select_algo(d, dtype, algo);
-  if (sel < 0)
-    return fail(DWM_EUNSUPPORTED,
-                "tcgen05 path needs float32, C %% 32 == 0 and F %% 64 == 0 (got C=%d F=%d)", d->c, d->f);
+  int sel = dwm_select_algo(d, dtype, algo);
+  if (sel == DWM_ALGO_SMALL_C) sel = algo == DWM_ALGO_AUTO ? DWM_ALGO_EXACT : -1;
+  if (sel < 0) return bad_algo(d, algo);
   if (sel == DWM_ALGO_TC)
     return launch_gemm_tc(*d, V, U, y, flag, (cudaStream_t)stream);
   return launch_gemm_exact(*d, dtype, V, U, y, flag, (cudaStream_t)stream);
+}
+
+int dwm_conv2d_small_c(const dwm_desc_t* d, const void* x, const void* U, void* y, int32_t* flag,
+                       void* stream) {
+  if (int st = check_common(d, DWM_F32)) return st;
+  if (!small_c_supported(*d)) return bad_algo(d, DWM_ALGO_SMALL_C);
+  return launch_small_c(*d, x, U, y, flag, (cudaStream_t)stream);
 }
 
 int dwm_conv2d_forward(const dwm_desc_t* d, int dtype, int algo, const void* x, const void* w,
                        void* y, void* ws, size_t ws_bytes, int32_t* flag, void* stream) {
   if (int st = check_common(d, dtype)) return st;
   const int sel = dwm_select_algo(d, dtype, algo);
-  if (sel < 0)
-    return fail(DWM_EUNSUPPORTED,
-                "tcgen05 path needs float32, C %% 32 == 0 and F %% 64 == 0 (got C=%d F=%d)", d->c, d->f);
+  if (sel < 0) return bad_algo(d, algo);
   const size_t need = dwm_workspace_bytes(d, dtype, sel);
   if (!ws || ws_bytes < need)
     return fail(DWM_EINVAL_SHAPE, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
   const size_t es = dtype == DWM_F64 ? 8 : 4;
-  const size_t v_bytes = (size_t)d->num_freqs * (size_t)d->tiles * (size_t)d->c * es;
   char* base = (char*)ws;
   void* V = base;
-  void* U = base + ((v_bytes + 255) / 256) * 256;
+  void* U = base + (sel == DWM_ALGO_SMALL_C ? 0 : round_up(v_bytes_of(d, es), 256));
   cudaStream_t s = (cudaStream_t)stream;
   int st;
   if (sel == DWM_ALGO_TC) {
@@ -176,6 +199,7 @@ int dwm_conv2d_forward(const dwm_desc_t* d, int dtype, int algo, const void* x, 
   } else {
     if ((st = launch_filter_transform(*d, dtype, w, U, s))) return st;
   }
+  if (sel == DWM_ALGO_SMALL_C) return launch_small_c(*d, x, U, y, flag, s);
   if ((st = launch_input_transform(*d, dtype, x, V, s))) return st;
   if (sel == DWM_ALGO_TC) return launch_gemm_tc(*d, V, U, y, flag, s);
   return launch_gemm_exact(*d, dtype, V, U, y, flag, s);

@@ -78,7 +78,11 @@ def test_exact_engine_matches_reference_golden(cuda, case):
     y32 = dwm_conv2d(d, g, spec, precision="binary32", algo="exact")
     ref32 = ARR[f"{case['name']}/dwm32"]
     assert y32.dtype == np.float32 and y32.shape == ref32.shape
-    if d.shape[1] <= 4:
+    n, c, h, w = d.shape
+    oh, ow = spec.out_dims(h, w)
+    if c <= 4 and n * (-(-oh // 2)) * (-(-ow // 2)) >= 4:
+        # bit-identical where the reference's BLAS runs a sequential GEMM
+        # (a single-tile batch makes NumPy dispatch a GEMV with its own order)
         assert np.array_equal(y32, ref32), np.max(np.abs(y32 - ref32))
     else:
         assert np.max(np.abs(y32 - ref32)) <= 4e-5 * max(1.0, np.max(np.abs(ref32)))
