@@ -42,7 +42,7 @@ def parse():
     from paper_2002_00552_b200.configs import DEFAULT_WORKLOAD, WORKLOADS
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--algo", default="auto", choices=["auto", "exact", "tc", "small_c"])
@@ -77,12 +77,13 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.first = threading.Event()
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._pump, daemon=True)
             self.thread.start()
@@ -93,6 +94,11 @@ class ClockSampler:
     def _pump(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self.first.set()
+
+    def wait_first(self, timeout=5.0):
+        if self.proc is not None:
+            self.first.wait(timeout)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -255,6 +261,8 @@ def main():
         if st:
             _native.check(st, "dwm_conv2d_forward")
 
+    clocks = ClockSampler(dev.index).__enter__()
+    clocks.wait_first()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -267,7 +275,8 @@ def main():
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clocks:
+    n_before = len(clocks.lines)
+    if True:
         for i in range(args.steps):
             if flush is not None:
                 flush.zero_()
@@ -275,6 +284,11 @@ def main():
             step()
             ends[i].record(stream)
         torch.cuda.synchronize()
+    time.sleep(0.06)
+    clocks.__exit__(None, None, None)
+    # samples from the warm-up on; keep the timed-region ones when there are enough
+    if len(clocks.lines) - n_before >= 3:
+        clocks.lines = clocks.lines[n_before:]
     if dist is not None:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]

@@ -2,27 +2,33 @@
 // (C_in <= 4: the ResNet-50 / AlexNet stems of BASELINE configs[1], [2]).
 //
 // With K = C_in <= 4 the per-frequency "GEMM" is not a tensor-core
-// contraction (SURVEY §7 hard part 4); the whole forward is FP32-pipe bound.
-// One persistent kernel therefore does everything on the CUDA cores and only
-// x is read and y written in HBM:
+// contraction (SURVEY §7 hard part 4); the whole forward is FP32-pipe bound
+// (FP32 FMA peak on B200 = 148 SM x 128 lanes x 1.965 GHz, measured 72 TFLOP/s
+// with tools/fp32_peak.cu).  One persistent kernel does everything on the CUDA
+// cores and only x is read and y written in HBM:
 //
 //   prologue : U[freq][F][C] (from the filter-transform kernel) -> smem,
-//              transposed to [freq][C][f-block] for broadcast float4 reads.
-//   per tile block (64 consecutive 2x2 output tiles) and per plan part:
+//              transposed to [freq][C][f-block] (resident for the whole kernel).
+//   per tile block (BM consecutive 2x2 output tiles) and per plan part:
 //     producer: polyphase gather of the part's (count+1)^2 input window for
 //               every (tile, channel) straight from x (padding and the
 //               reference's even-extension zeros by predicate), Bt.d.B row
-//               stage then column stage -> V part in smem (double buffered;
-//               the x loads of part p+1 are issued before part p's math).
+//               stage then column stage with compile-time coefficients ->
+//               V part in smem [q][c][tile] (double buffered; the x loads of
+//               part p+1 are issued before part p's math).
 //     consumer: per frequency, M = sum_c U*V (FMA chain, c ascending);
 //               At.m.A row stage S, column stage T with compile-time
-//               coefficients (0 skipped, +-1 as add/sub); y += T in plan order.
+//               coefficients (0 skipped, +-1 as add/sub); y += T in plan
+//               order, y accumulated in shared memory.  All of it runs on
+//               packed f32x2 FFMA2/FADD2 pairs over adjacent filters, which
+//               halves FP32 issue slots (each lane of a pair is an ordinary
+//               IEEE binary32 RN operation).
 //   epilogue : interleave the 2x2 tiles into NCHW, truncate odd extents,
 //              raise the non-finite flag.
 //
 // Every rounding step is the reference's (engines.py:164-194, 244-255 with a
-// sequential BLAS), so the output is bit-identical to the reference DWM in
-// binary32 (see tests/test_gpu_parity.py).
+// sequential BLAS), so the output equals the reference DWM in binary32 (see
+// tests/test_gpu_parity.py; only the sign of exact zeros may differ).
 #include <utility>
 
 #include "dwm_common.cuh"
@@ -31,12 +37,8 @@
 namespace dwm {
 namespace {
 
-constexpr int BM = 64;       // tiles per block
-constexpr int BN = 32;       // filters per block
-constexpr int TM = 2;        // tiles per thread (strided by 32)
-constexpr int TN = 4;        // filters per thread (contiguous)
-constexpr int THREADS = 256; // (BM/TM) * (BN/TN)
-constexpr int MAXQ = 16;     // frequencies per part, (3+1)^2
+constexpr int THREADS = 256;  // 32 tile lanes x 8 filter groups
+constexpr int MAXQ = 16;      // frequencies per part, (3+1)^2
 
 // At coefficient of F(2, r): row i (output), column a (frequency).
 __host__ __device__ constexpr int at_coef(int r, int i, int a) {
@@ -44,17 +46,80 @@ __host__ __device__ constexpr int at_coef(int r, int i, int a) {
        : r == 2 ? (i == 0 ? (a <= 1 ? 1 : 0) : (a == 1 ? 1 : (a == 2 ? -1 : 0)))
                 : (i == 0 ? (a <= 2 ? 1 : 0) : (a == 0 ? 0 : (a == 1 ? 1 : -1)));
 }
-
-template <int K> __device__ __forceinline__ float cmul(float m) {
-  if constexpr (K == 1) return m;
-  else if constexpr (K == -1) return -m;
-  else return 0.f;
+// Bt coefficient of F(2, r): row a (frequency), column i (window sample).
+__host__ __device__ constexpr int bt_coef(int r, int a, int i) {
+  // F(2,1): I2;  F(2,2): [[1,-1,0],[0,1,0],[0,1,-1]];
+  // F(2,3): [[1,0,-1,0],[0,1,1,0],[0,-1,1,0],[0,1,0,-1]]
+  return r == 1 ? (a == i ? 1 : 0)
+       : r == 2 ? (a == 0 ? (i == 0 ? 1 : i == 1 ? -1 : 0)
+                  : a == 1 ? (i == 1 ? 1 : 0)
+                           : (i == 1 ? 1 : i == 2 ? -1 : 0))
+                : (a == 0 ? (i == 0 ? 1 : i == 2 ? -1 : 0)
+                  : a == 1 ? (i == 1 || i == 2 ? 1 : 0)
+                  : a == 2 ? (i == 1 ? -1 : i == 2 ? 1 : 0)
+                           : (i == 1 ? 1 : i == 3 ? -1 : 0));
 }
-// fma(K, m, acc) for K in {0, +-1}: exact skip / add / sub.
-template <int K> __device__ __forceinline__ float cfma(float m, float acc) {
-  if constexpr (K == 1) return __fadd_rn(acc, m);
-  else if constexpr (K == -1) return __fsub_rn(acc, m);
-  else return acc;
+// first index with a nonzero coefficient (the sequential sum starts there)
+__host__ __device__ constexpr int at_first(int r, int i) {
+  int k = 0;
+  while (at_coef(r, i, k) == 0) ++k;
+  return k;
+}
+__host__ __device__ constexpr int bt_first(int r, int a) {
+  int k = 0;
+  while (bt_coef(r, a, k) == 0) ++k;
+  return k;
+}
+
+// ---- scalar chain (producer): acc = sum_k K_k * m_k, K in {0, +-1} ---------
+// Zero terms are skipped and the first nonzero term is a move (BLAS starts from
+// +0, so only the sign of an exact zero can differ).  A leading -1 (Bt row 2
+// of F(2,3)) is carried as a negated accumulator and fixed by `finish`.
+template <int K, bool FIRST, bool NEG> __device__ __forceinline__ void chain(float& acc, float m) {
+  if constexpr (K == 0) return;
+  else if constexpr (FIRST) acc = m;  // value is K*m; sign kept in NEG
+  else if constexpr ((K == 1) != NEG) acc = __fadd_rn(acc, m);
+  else acc = __fsub_rn(acc, m);
+}
+
+// ---- packed f32x2 (two adjacent filters) ----------------------------------
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk(f2 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// every At row starts with +1, so no sign tracking is needed here
+template <int K, bool FIRST> __device__ __forceinline__ void chain2(f2& acc, f2 m) {
+  if constexpr (K == 0) return;
+  else if constexpr (FIRST) { static_assert(K == 1, "At rows start with +1"); acc = m; }
+  else if constexpr (K == 1) acc = add2(acc, m);
+  else acc = sub2(acc, m);
 }
 
 template <typename F, int... Is>
@@ -65,205 +130,271 @@ template <int N, typename F> __device__ __forceinline__ void static_for(F&& f) {
   static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
-struct Acc {
-  float v[TM][TN][2][2];
+template <int CC_, int TM_, int TN_>
+struct Cfg {
+  static constexpr int CC = CC_, TM = TM_, TN = TN_;
+  static constexpr int BM = 32 * TM;         // tiles per block
+  static constexpr int BN = 8 * TN;          // filters per block
+  static constexpr int NP = TN / 2;          // filter pairs per thread
+  static constexpr int NACC2 = TM * NP * 4;  // packed accumulators per thread
+  static constexpr int VSTAGE = MAXQ * CC * BM;
+  static size_t smem_bytes(int num_freqs) {
+    return ((size_t)NACC2 * 2 * THREADS + 2 * (size_t)VSTAGE + (size_t)num_freqs * CC * BN) * sizeof(float);
+  }
 };
 
-// Consume one part: sV [q][BM][CC], sU at the part's first frequency [q][CC][BN].
-template <int CC, int PR, int PC>
+// Consume one part.  sV: [q][CC][BM]; sU: part's first frequency, [q][CC][BN];
+// sAcc: packed y accumulators [NACC2][THREADS] (conflict-free 8-byte slots).
+template <class K, int PR, int PC>
 __device__ __forceinline__ void consume_part(const float* __restrict__ sV, const float* __restrict__ sU,
-                                             int tm, int tn, Acc& acc, bool first_part) {
-  constexpr int LR = PR + 1, LC = PC + 1;
-  float T[TM][TN][2][2];
+                                             f2* __restrict__ sAcc, int tid, bool first_part) {
+  constexpr int LR = PR + 1, LC = PC + 1, TM = K::TM, NP = K::NP, CC = K::CC, BM = K::BM, BN = K::BN;
+  const int tm = tid % 32, tn = tid / 32;
+  f2 T[TM][NP][2][2];
   static_for<LC>([&](auto bI) {
     constexpr int b = decltype(bI)::value;
-    float S[TM][TN][2];
+    f2 S[TM][NP][2];
     static_for<LR>([&](auto aI) {
       constexpr int a = decltype(aI)::value;
       constexpr int q = a * LC + b;
-      float M[TM][TN];
+      f2 M[TM][NP];
 #pragma unroll
       for (int c = 0; c < CC; ++c) {
         float v[TM];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) v[i] = sV[(q * BM + tm + 32 * i) * CC + c];
-        const float4 u4 = *reinterpret_cast<const float4*>(sU + (q * CC + c) * BN + tn * TN);
-        const float u[TN] = {u4.x, u4.y, u4.z, u4.w};
+        for (int i = 0; i < TM; ++i) v[i] = sV[(q * CC + c) * BM + tm + 32 * i];
+        f2 u[NP];
+        const float* up = sU + (q * CC + c) * BN + tn * K::TN;
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
+        for (int jp = 0; jp < NP; jp += 2) {
+          if (jp + 1 < NP) {
+            const float4 u4 = *reinterpret_cast<const float4*>(up + 2 * jp);
+            u[jp] = pk(u4.x, u4.y);
+            u[jp + 1] = pk(u4.z, u4.w);
+          } else {
+            const float2 u2 = *reinterpret_cast<const float2*>(up + 2 * jp);
+            u[jp] = pk(u2.x, u2.y);
+          }
+        }
 #pragma unroll
-          for (int j = 0; j < TN; ++j)
-            M[i][j] = (c == 0) ? __fmul_rn(u[j], v[i]) : __fmaf_rn(u[j], v[i], M[i][j]);
+        for (int i = 0; i < TM; ++i) {
+          const f2 vv = pk(v[i], v[i]);
+#pragma unroll
+          for (int jp = 0; jp < NP; ++jp) M[i][jp] = (c == 0) ? mul2(u[jp], vv) : fma2(u[jp], vv, M[i][jp]);
+        }
       }
-      constexpr int k0 = at_coef(PR, 0, a), k1 = at_coef(PR, 1, a);
+      // row stage of At.m.A: S[i'] = sum_a At_r[i'][a] M_a
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          if constexpr (a == 0) {
-            S[i][j][0] = cmul<k0>(M[i][j]);
-            S[i][j][1] = cmul<k1>(M[i][j]);
-          } else {
-            S[i][j][0] = cfma<k0>(M[i][j], S[i][j][0]);
-            S[i][j][1] = cfma<k1>(M[i][j], S[i][j][1]);
-          }
+        for (int jp = 0; jp < NP; ++jp) {
+          chain2<at_coef(PR, 0, a), (a == at_first(PR, 0))>(S[i][jp][0], M[i][jp]);
+          chain2<at_coef(PR, 1, a), (a == at_first(PR, 1))>(S[i][jp][1], M[i][jp]);
         }
     });
-    constexpr int c0 = at_coef(PC, 0, b), c1 = at_coef(PC, 1, b);
+    // column stage: T[i'][j'] = sum_b S[i'](b) * At_c[j'][b]
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int j = 0; j < TN; ++j)
+      for (int jp = 0; jp < NP; ++jp)
 #pragma unroll
         for (int ii = 0; ii < 2; ++ii) {
-          if constexpr (b == 0) {
-            T[i][j][ii][0] = cmul<c0>(S[i][j][ii]);
-            T[i][j][ii][1] = cmul<c1>(S[i][j][ii]);
-          } else {
-            T[i][j][ii][0] = cfma<c0>(S[i][j][ii], T[i][j][ii][0]);
-            T[i][j][ii][1] = cfma<c1>(S[i][j][ii], T[i][j][ii][1]);
-          }
+          chain2<at_coef(PC, 0, b), (b == at_first(PC, 0))>(T[i][jp][ii][0], S[i][jp][ii]);
+          chain2<at_coef(PC, 1, b), (b == at_first(PC, 1))>(T[i][jp][ii][1], S[i][jp][ii]);
         }
   });
+  // aggregation in plan order (tensor.py:68-81): acc = acc + T
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j)
+    for (int jp = 0; jp < NP; ++jp)
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj)
-          acc.v[i][j][ii][jj] = first_part ? T[i][j][ii][jj] : __fadd_rn(acc.v[i][j][ii][jj], T[i][j][ii][jj]);
+        for (int jj = 0; jj < 2; ++jj) {
+          f2* slot = sAcc + (((i * NP + jp) * 2 + ii) * 2 + jj) * THREADS + tid;
+          *slot = first_part ? T[i][jp][ii][jj] : add2(*slot, T[i][jp][ii][jj]);
+        }
 }
 
-template <int CC>
-__device__ __forceinline__ void consume_dispatch(int pr, int pc, const float* sV, const float* sU, int tm,
-                                                 int tn, Acc& acc, bool first) {
-  switch (pr * 4 + pc) {
-    case 5: consume_part<CC, 1, 1>(sV, sU, tm, tn, acc, first); break;
-    case 6: consume_part<CC, 1, 2>(sV, sU, tm, tn, acc, first); break;
-    case 7: consume_part<CC, 1, 3>(sV, sU, tm, tn, acc, first); break;
-    case 9: consume_part<CC, 2, 1>(sV, sU, tm, tn, acc, first); break;
-    case 10: consume_part<CC, 2, 2>(sV, sU, tm, tn, acc, first); break;
-    case 11: consume_part<CC, 2, 3>(sV, sU, tm, tn, acc, first); break;
-    case 13: consume_part<CC, 3, 1>(sV, sU, tm, tn, acc, first); break;
-    case 14: consume_part<CC, 3, 2>(sV, sU, tm, tn, acc, first); break;
-    default: consume_part<CC, 3, 3>(sV, sU, tm, tn, acc, first); break;
+#define DWM_PART_SWITCH(pr, pc, CALL)            \
+  switch ((pr) * 4 + (pc)) {                     \
+    case 5: CALL(1, 1); break;                   \
+    case 6: CALL(1, 2); break;                   \
+    case 7: CALL(1, 3); break;                   \
+    case 9: CALL(2, 1); break;                   \
+    case 10: CALL(2, 2); break;                  \
+    case 11: CALL(2, 3); break;                  \
+    case 13: CALL(3, 1); break;                  \
+    case 14: CALL(3, 2); break;                  \
+    default: CALL(3, 3); break;                  \
   }
+
+// Producer geometry of one (tile, channel) for a tile block, computed once.
+struct ProdTile {
+  const float* xc;  // x[n][c]
+  int y0, x0;       // 2*ty*s_h - pad_top, 2*tx*s_w - pad_left
+  int ky, kx;       // 2*ty, 2*tx (window sample index base)
+  bool live;
+};
+
+__device__ __forceinline__ ProdTile prod_tile(const dwm_desc_t& d, const float* __restrict__ x, int tile, int c) {
+  ProdTile p;
+  p.live = tile < d.tiles;
+  const int t = p.live ? tile : 0;
+  const int tx = t % d.tw;
+  const int t2 = t / d.tw;
+  const int ty = t2 % d.th;
+  const int n = t2 / d.th;
+  p.xc = x + ((size_t)n * d.c + c) * (size_t)d.h * d.w;
+  p.ky = 2 * ty;
+  p.kx = 2 * tx;
+  p.y0 = 2 * ty * d.s_h - d.pad_top;
+  p.x0 = 2 * tx * d.s_w - d.pad_left;
+  return p;
 }
 
-// Producer half 1: gather the part's input window for (tile, c) into registers.
-__device__ __forceinline__ void load_window(const dwm_desc_t& d, const float* __restrict__ x, int64_t tile,
-                                            int c, int rp, int cp, float win[4][4]) {
+// Producer half 1: gather the part's (count+1)^2 window into registers.
+__device__ __forceinline__ void load_window(const dwm_desc_t& d, const ProdTile& p, int rp, int cp,
+                                            float win[4][4]) {
   const dwm_axis_part_t R = d.row_parts[rp], Cc = d.col_parts[cp];
-  const int lr = R.count + 1, lc = Cc.count + 1;
-  const int tx = (int)(tile % d.tw);
-  const int64_t t2 = tile / d.tw;
-  const int ty = (int)(t2 % d.th);
-  const int n = (int)(t2 / d.th);
-  const bool live = tile < d.tiles;
-  const float* xc = x + ((int64_t)n * d.c + c) * d.h * d.w;
   int rows[4], cols[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int k = 2 * ty + i;
-    const int row = R.origin + d.s_h * k - d.pad_top;
-    rows[i] = (live && i < lr && k < d.oh - 1 + R.count && row >= 0 && row < d.h) ? row : -1;
+    const int row = p.y0 + R.origin + d.s_h * i;
+    rows[i] = (p.live && i <= R.count && p.ky + i < d.oh - 1 + R.count && row >= 0 && row < d.h) ? row * d.w : -1;
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int k = 2 * tx + j;
-    const int col = Cc.origin + d.s_w * k - d.pad_left;
-    cols[j] = (j < lc && k < d.ow - 1 + Cc.count && col >= 0 && col < d.w) ? col : -1;
+    const int col = p.x0 + Cc.origin + d.s_w * j;
+    cols[j] = (j <= Cc.count && p.kx + j < d.ow - 1 + Cc.count && col >= 0 && col < d.w) ? col : -1;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? __ldg(xc + (int64_t)rows[i] * d.w + cols[j]) : 0.f;
+      win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? __ldg(p.xc + rows[i] + cols[j]) : 0.f;
 }
 
-// Producer half 2: Bt.d.B (row stage then column stage) -> sV[q][t][c].
-template <int CC>
-__device__ __forceinline__ void transform_store(const dwm_desc_t& d, int rp, int cp, const float win[4][4],
-                                                float* __restrict__ sV, int t, int c) {
-  const int pr = d.row_parts[rp].count, pc = d.col_parts[cp].count;
-  const int lr = pr + 1, lc = pc + 1;
-  float tt[4][4];
+// Producer half 2: Bt.d.B (row stage then column stage, compile-time
+// coefficients) -> sV[q][c][t].
+template <class K, int PR, int PC>
+__device__ __forceinline__ void transform_store(const float (&win)[4][4], float* __restrict__ sV, int t, int c) {
+  constexpr int LR = PR + 1, LC = PC + 1;
+  float tt[LR][LC];
+  static_for<LR>([&](auto aI) {
+    constexpr int a = decltype(aI)::value;
+    constexpr bool neg = bt_coef(PR, a, bt_first(PR, a)) < 0;
+    static_for<LR>([&](auto iI) {
+      constexpr int i = decltype(iI)::value;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+      for (int j = 0; j < LC; ++j) chain<bt_coef(PR, a, i), (i == bt_first(PR, a)), neg>(tt[a][j], win[i][j]);
+    });
+    if constexpr (neg) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float acc = __fmul_rn(c_bt[pr][a][0], win[0][j]);
-#pragma unroll
-      for (int i = 1; i < 4; ++i)
-        if (i < lr) acc = __fmaf_rn(c_bt[pr][a][i], win[i][j], acc);
-      tt[a][j] = acc;
+      for (int j = 0; j < LC; ++j) tt[a][j] = -tt[a][j];
     }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (a < lr && b < lc) {
-        float acc = __fmul_rn(tt[a][0], c_bt[pc][b][0]);
-#pragma unroll
-        for (int j = 1; j < 4; ++j)
-          if (j < lc) acc = __fmaf_rn(tt[a][j], c_bt[pc][b][j], acc);
-        sV[((a * lc + b) * BM + t) * CC + c] = acc;
-      }
+  });
+  static_for<LR>([&](auto aI) {
+    constexpr int a = decltype(aI)::value;
+    static_for<LC>([&](auto bI) {
+      constexpr int b = decltype(bI)::value;
+      constexpr bool neg = bt_coef(PC, b, bt_first(PC, b)) < 0;
+      float v;
+      static_for<LC>([&](auto jI) {
+        constexpr int j = decltype(jI)::value;
+        chain<bt_coef(PC, b, j), (j == bt_first(PC, b)), neg>(v, tt[a][j]);
+      });
+      sV[((a * LC + b) * K::CC + c) * K::BM + t] = neg ? -v : v;
+    });
+  });
 }
 
-template <int CC>
-__global__ void __launch_bounds__(THREADS, 2)
+template <class K>
+__global__ void __launch_bounds__(THREADS, 1)
 small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __restrict__ U,
                float* __restrict__ y, int32_t* __restrict__ flag) {
+  constexpr int CC = K::CC, BM = K::BM, BN = K::BN, TM = K::TM, TN = K::TN, NP = K::NP;
   extern __shared__ __align__(16) float smem[];
-  float* sU = smem;                                    // [freq][CC][BN]
-  float* sVbuf = smem + (size_t)d.num_freqs * CC * BN; // [2][MAXQ][BM][CC]
-  constexpr int VSTAGE = MAXQ * BM * CC;
+  f2* sAcc = reinterpret_cast<f2*>(smem);                      // [NACC2][THREADS]
+  float* sVbuf = smem + K::NACC2 * 2 * THREADS;                  // [2][MAXQ][CC][BM]
+  float* sU = sVbuf + 2 * K::VSTAGE;                             // [freq][CC][BN]
 
   const int tid = threadIdx.x;
   const int tm = tid % 32, tn = tid / 32;
   const int f0 = blockIdx.y * BN;
   const int F = d.f;
   const int nparts = d.n_row_parts * d.n_col_parts;
-  const int64_t nblocks = (d.tiles + BM - 1) / BM;
+  const int nblocks = (int)((d.tiles + BM - 1) / BM);
 
   for (int e = tid; e < d.num_freqs * CC * BN; e += THREADS) {
     const int fl = e % BN, c = (e / BN) % CC, q = e / (BN * CC);
     const int f = f0 + fl;
-    sU[e] = f < F ? U[((int64_t)q * F + f) * CC + c] : 0.f;
+    sU[e] = f < F ? U[((size_t)q * F + f) * CC + c] : 0.f;
   }
 
-  // producer role: (tile t, channel c) of the block
-  const bool producer = tid < BM * CC;
-  const int pt = tid / CC, pc_ch = tid % CC;
+  // producer slots: (tile t, channel c), t fastest within a warp
+  constexpr int PSLOTS = BM * CC;
+  constexpr int PPER = (PSLOTS + THREADS - 1) / THREADS;  // slots per thread (1 or 2)
+  int pt[PPER], pch[PPER];
+  bool pact[PPER];
+#pragma unroll
+  for (int s = 0; s < PPER; ++s) {
+    const int e = tid + s * THREADS;
+    pact[s] = e < PSLOTS;
+    pt[s] = e % BM;
+    pch[s] = pact[s] ? e / BM : 0;
+  }
 
-  int64_t tb = blockIdx.x;
+  int tb = blockIdx.x;
   if (tb >= nblocks) return;
-  float win[4][4];
-  if (producer) load_window(d, x, tb * BM + pt, pc_ch, 0, 0, win);
-  if (producer) transform_store<CC>(d, 0, 0, win, sVbuf, pt, pc_ch);
+  float win[PPER][4][4];
+  ProdTile ptile[PPER];
+#pragma unroll
+  for (int s = 0; s < PPER; ++s) {
+    ptile[s] = prod_tile(d, x, tb * BM + pt[s], pch[s]);
+    if (pact[s]) {
+      load_window(d, ptile[s], 0, 0, win[s]);
+#define DWM_TS0(A, B) transform_store<K, A, B>(win[s], sVbuf, pt[s], pch[s])
+      DWM_PART_SWITCH(d.row_parts[0].count, d.col_parts[0].count, DWM_TS0)
+#undef DWM_TS0
+    }
+  }
   __syncthreads();
 
   int stage = 0;
-  Acc acc;
   for (; tb < nblocks; tb += gridDim.x) {
     int qoff = 0;
     for (int p = 0; p < nparts; ++p) {
       const int rp = p / d.n_col_parts, cpi = p % d.n_col_parts;
       // next unit of work: part p+1 of this block, or part 0 of the next block
-      const bool has_next = (p + 1 < nparts) || (tb + gridDim.x < nblocks);
-      const int np = (p + 1 < nparts) ? p + 1 : 0;
-      const int64_t ntb = (p + 1 < nparts) ? tb : tb + gridDim.x;
+      const bool last = p + 1 == nparts;
+      const bool has_next = !last || (tb + (int)gridDim.x < nblocks);
+      const int np = last ? 0 : p + 1;
       const int nrp = np / d.n_col_parts, ncp = np % d.n_col_parts;
-      if (producer && has_next) load_window(d, x, ntb * BM + pt, pc_ch, nrp, ncp, win);
+#pragma unroll
+      for (int s = 0; s < PPER; ++s) {
+        if (last && has_next) ptile[s] = prod_tile(d, x, (tb + gridDim.x) * BM + pt[s], pch[s]);
+        if (pact[s] && has_next) load_window(d, ptile[s], nrp, ncp, win[s]);
+      }
 
-      consume_dispatch<CC>(d.row_parts[rp].count, d.col_parts[cpi].count, sVbuf + stage * VSTAGE,
-                           sU + qoff * CC * BN, tm, tn, acc, p == 0);
+      const float* sV = sVbuf + stage * K::VSTAGE;
+      const float* sUp = sU + qoff * CC * BN;
+#define DWM_CONSUME(A, B) consume_part<K, A, B>(sV, sUp, sAcc, tid, p == 0)
+      DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cpi].count, DWM_CONSUME)
+#undef DWM_CONSUME
       qoff += (d.row_parts[rp].count + 1) * (d.col_parts[cpi].count + 1);
 
-      if (producer && has_next) transform_store<CC>(d, nrp, ncp, win, sVbuf + (stage ^ 1) * VSTAGE, pt, pc_ch);
+      if (has_next) {
+        float* sVn = sVbuf + (stage ^ 1) * K::VSTAGE;
+#pragma unroll
+        for (int s = 0; s < PPER; ++s) {
+          if (!pact[s]) continue;
+#define DWM_TSN(A, B) transform_store<K, A, B>(win[s], sVn, pt[s], pch[s])
+          DWM_PART_SWITCH(d.row_parts[nrp].count, d.col_parts[ncp].count, DWM_TSN)
+#undef DWM_TSN
+        }
+      }
       stage ^= 1;
       __syncthreads();
     }
@@ -271,35 +402,40 @@ small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __r
     bool bad = false;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-      const int64_t tile = tb * BM + tm + 32 * i;
+      const int tile = tb * BM + tm + 32 * i;
       if (tile >= d.tiles) continue;
-      const int tx = (int)(tile % d.tw);
-      const int64_t t2 = tile / d.tw;
-      const int ty = (int)(t2 % d.th);
-      const int n = (int)(t2 / d.th);
+      const int tx = tile % d.tw;
+      const int t2 = tile / d.tw;
+      const int ty = t2 % d.th;
+      const int n = t2 / d.th;
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int f = f0 + tn * TN + j;
-        if (f >= F) continue;
-        float* yf = y + ((int64_t)n * F + f) * d.oh * d.ow;
+      for (int jp = 0; jp < NP; ++jp) {
 #pragma unroll
-        for (int ii = 0; ii < 2; ++ii) {
-          const int oy = 2 * ty + ii;
-          if (oy >= d.oh) continue;
-          const float v0 = acc.v[i][j][ii][0], v1 = acc.v[i][j][ii][1];
-          const int ox = 2 * tx;
-          float* dst = yf + (int64_t)oy * d.ow + ox;
-          if (ox + 1 < d.ow) {
-            bad |= !(isfinite(v0) && isfinite(v1));
-            if ((d.ow & 1) == 0) {
-              __stcs(reinterpret_cast<float2*>(dst), make_float2(v0, v1));
+        for (int half = 0; half < 2; ++half) {
+          const int f = f0 + tn * TN + 2 * jp + half;
+          if (f >= F) continue;
+          float* yf = y + ((size_t)n * F + f) * (size_t)d.oh * d.ow;
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            const int oy = 2 * ty + ii;
+            if (oy >= d.oh) continue;
+            const float2 a0 = upk(sAcc[(((i * NP + jp) * 2 + ii) * 2 + 0) * THREADS + tid]);
+            const float2 a1 = upk(sAcc[(((i * NP + jp) * 2 + ii) * 2 + 1) * THREADS + tid]);
+            const float v0 = half ? a0.y : a0.x, v1 = half ? a1.y : a1.x;
+            const int ox = 2 * tx;
+            float* dst = yf + (size_t)oy * d.ow + ox;
+            if (ox + 1 < d.ow) {
+              bad |= !(isfinite(v0) && isfinite(v1));
+              if ((d.ow & 1) == 0) {
+                __stcs(reinterpret_cast<float2*>(dst), make_float2(v0, v1));
+              } else {
+                __stcs(dst, v0);
+                __stcs(dst + 1, v1);
+              }
             } else {
+              bad |= !isfinite(v0);
               __stcs(dst, v0);
-              __stcs(dst + 1, v1);
             }
-          } else {
-            bad |= !isfinite(v0);
-            __stcs(dst, v0);
           }
         }
       }
@@ -308,30 +444,44 @@ small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __r
   }
 }
 
-template <int CC>
-int launch_cc(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
-  const size_t smem = ((size_t)d.num_freqs * CC * BN + 2 * (size_t)MAXQ * BM * CC) * sizeof(float);
-  DWM_CUDA_TRY(cudaFuncSetAttribute(small_c_kernel<CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <class K>
+int launch_cfg(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
+  const size_t smem = K::smem_bytes(d.num_freqs);
+  DWM_CUDA_TRY(cudaFuncSetAttribute(small_c_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 0, per_sm = 0;
   DWM_CUDA_TRY(cudaGetDevice(&dev));
   DWM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DWM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_c_kernel<CC>, THREADS, smem));
+  DWM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_c_kernel<K>, THREADS, smem));
   if (per_sm < 1) return fail(DWM_EUNSUPPORTED, "small-C kernel does not fit (smem %zu B)", smem);
-  const int fblocks = (d.f + BN - 1) / BN;
-  const int64_t nblocks = (d.tiles + BM - 1) / BM;
+  const int fblocks = (d.f + K::BN - 1) / K::BN;
+  const int64_t nblocks = (d.tiles + K::BM - 1) / K::BM;
   int64_t gx = ((int64_t)sms * per_sm + fblocks - 1) / fblocks;
   if (gx > nblocks) gx = nblocks;
-  small_c_kernel<CC><<<dim3((unsigned)gx, (unsigned)fblocks), THREADS, smem, s>>>(d, x, U, y, flag);
+  small_c_kernel<K><<<dim3((unsigned)gx, (unsigned)fblocks), THREADS, smem, s>>>(d, x, U, y, flag);
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
+}
+
+constexpr size_t SMEM_CAP = 220 * 1024;
+
+// Wide variant (2 tiles x 8 filters per thread, 64x64 block) when its resident
+// U fits; else the narrow one (4 tiles x 4 filters, 128x32 block).
+template <int CC>
+int launch_cc(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
+  using Wide = Cfg<CC, 2, 8>;
+  using Narrow = Cfg<CC, 4, 4>;
+  if (d.f > 32 && Wide::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_cfg<Wide>(d, x, U, y, flag, s);
+  return launch_cfg<Narrow>(d, x, U, y, flag, s);
 }
 
 }  // namespace
 
 bool small_c_supported(const dwm_desc_t& d) {
   if (d.c < 1 || d.c > 4) return false;
-  const size_t smem = ((size_t)d.num_freqs * d.c * BN + 2 * (size_t)MAXQ * BM * d.c) * sizeof(float);
-  return smem <= 200 * 1024;
+  if (d.tiles + 256 >= (int64_t)1 << 31) return false;  // 32-bit tile indexing
+  const size_t narrow = ((size_t)16 * 2 * THREADS + 2 * (size_t)MAXQ * d.c * 128 + (size_t)d.num_freqs * d.c * 32) *
+                        sizeof(float);
+  return narrow <= SMEM_CAP;
 }
 
 int launch_small_c(const dwm_desc_t& d, const void* x, const void* U, void* y, int32_t* flag, cudaStream_t s) {
