@@ -151,45 +151,99 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
     _check_plan_matches(plan, desc)
 
     from_numpy = not _is_torch(data)
-    if from_numpy:
-        dev = torch.device("cuda", torch.cuda.current_device())
-        x_d = torch.from_numpy(np.ascontiguousarray(data)).to(dev, dtype=tdt)
-    else:
-        dev = data.device if data.is_cuda else torch.device("cuda", torch.cuda.current_device())
-        x_d = data.to(dev, dtype=tdt, non_blocking=True).contiguous()
+    host_in = from_numpy or not data.is_cuda
+    dev = (data.device if (not from_numpy and data.is_cuda)
+           else torch.device("cuda", torch.cuda.current_device()))
     w_d = (torch.from_numpy(np.ascontiguousarray(weights)) if not _is_torch(weights)
            else weights).to(dev, dtype=tdt).contiguous()
-
     oh, ow = desc.oh, desc.ow
     if out is not None:
         if tuple(out.shape) != (n, f, oh, ow) or out.dtype != tdt or not out.is_contiguous():
             raise ValueError(f"out must be a contiguous {(n, f, oh, ow)} {tdt} tensor")
-        y_d = out if out.is_cuda else torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
-    else:
-        y_d = torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
     algo_code = _native.ALGOS[algo]
-    ws_bytes = lib.dwm_workspace_bytes(desc, code, algo_code)
+
     with torch.cuda.device(dev):
         s = stream if stream is not None else torch.cuda.current_stream(dev)
-        ws = _workspace(dev, ws_bytes)
         flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
-        st = lib.dwm_conv2d_forward(desc, code, algo_code, x_d.data_ptr(), w_d.data_ptr(),
-                                    y_d.data_ptr(), ws.data_ptr(), ws_bytes,
-                                    flag.data_ptr() if flag is not None else None,
-                                    s.cuda_stream)
-        _native.check(st, "dwm_conv2d_forward")
+        if host_in:
+            x_h = (torch.from_numpy(np.ascontiguousarray(data)) if from_numpy else data.contiguous())
+            if x_h.dtype != tdt:
+                x_h = x_h.to(tdt)
+            if out is not None and not out.is_cuda:
+                y_h = out
+            else:
+                y_h = torch.empty((n, f, oh, ow), dtype=tdt, pin_memory=True)
+            _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
+            y_res = y_h
+        else:
+            x_d = data.to(dev, dtype=tdt).contiguous()
+            y_d = out if out is not None else torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
+            ws_bytes = lib.dwm_workspace_bytes(desc, code, algo_code)
+            ws = _workspace(dev, ws_bytes)
+            st = lib.dwm_conv2d_forward(desc, code, algo_code, x_d.data_ptr(), w_d.data_ptr(),
+                                        y_d.data_ptr(), ws.data_ptr(), ws_bytes,
+                                        flag.data_ptr() if flag is not None else None,
+                                        s.cuda_stream)
+            _native.check(st, "dwm_conv2d_forward")
+            y_res = y_d
         if counter is not None:
             counter.elementwise += int(lib.dwm_elementwise_count(desc))
         if check_finite and int(flag.item()) != 0:
             raise FloatingPointError("dwm_conv2d produced non-finite values")
-    if out is not None and not out.is_cuda:
-        out.copy_(y_d)
-        return out
     if from_numpy:
-        return y_d.cpu().numpy()
-    if not data.is_cuda:
-        return y_d.cpu()
-    return y_d
+        return y_res.numpy()
+    return y_res
+
+
+_SIDE_STREAMS = {}
+
+
+def _side_streams(dev):
+    torch = _torch()
+    if dev not in _SIDE_STREAMS:
+        _SIDE_STREAMS[dev] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _SIDE_STREAMS[dev]
+
+
+def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev):
+    """Host-resident input/output: the batch is cut into chunks whose
+    host->device copy, forward and device->host copy run on three streams, so
+    PCIe traffic in both directions overlaps the kernels (images are
+    independent, so chunking changes no result bit)."""
+    torch = _torch()
+    n = x_h.shape[0]
+    chunks = 1 if n < 2 else min(8, n)
+    bounds = [round(i * n / chunks) for i in range(chunks + 1)]
+    x_d = torch.empty(x_h.shape, dtype=x_h.dtype, device=dev)
+    y_d = torch.empty(y_h.shape, dtype=y_h.dtype, device=dev)
+    s_in, s_out = _side_streams(dev)
+    s_in.wait_stream(s)
+    ws_bytes = max(lib.dwm_workspace_bytes(_native.make_desc(
+        b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad), code, algo_code)
+        for b0, b1 in zip(bounds, bounds[1:]))
+    ws = _workspace(dev, ws_bytes)
+    for b0, b1 in zip(bounds, bounds[1:]):
+        with torch.cuda.stream(s_in):
+            x_d[b0:b1].copy_(x_h[b0:b1], non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+        s.wait_event(ev_in)
+        dk = _native.make_desc(b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad)
+        st = lib.dwm_conv2d_forward(dk, code, algo_code, x_d[b0].data_ptr(), w_d.data_ptr(),
+                                    y_d[b0].data_ptr(), ws.data_ptr(), ws_bytes,
+                                    flag.data_ptr() if flag is not None else None, s.cuda_stream)
+        _native.check(st, "dwm_conv2d_forward")
+        ev_done = torch.cuda.Event()
+        ev_done.record(s)
+        s_out.wait_event(ev_done)
+        with torch.cuda.stream(s_out):
+            y_h[b0:b1].copy_(y_d[b0:b1], non_blocking=True)
+    # device buffers are freed to torch's caching allocator only after the
+    # side streams are done with them
+    x_d.record_stream(s_in)
+    y_d.record_stream(s_out)
+    s.wait_stream(s_out)
+    s_out.synchronize()
 
 
 def convolve(data, weights, spec: ConvSpec, algo: str = "dwm", precision=None,
