@@ -43,7 +43,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     objs = []
     for src in srcs:
         obj = OUT_DIR / (src.stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("DWM_NVCC_FLAGS", "").split()
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

@@ -32,7 +32,7 @@ pytestmark = pytest.mark.gpu
 CASES = json.loads((GOLDEN / "cases.json").read_text())
 ARR = np.load(GOLDEN / "small_cases.npz")
 BASE = json.loads((GOLDEN / "baseline_samples.json").read_text())
-MSE_TOL = {"exact": 1.02, "tc": 1.0}
+MSE_TOL = {"exact": 1.02, "tc": 1.0, "small_c": 1.0}
 
 
 def _spec(case):
@@ -107,6 +107,48 @@ def test_baseline_workload_accuracy_exact(cuda, name):
     idx = tuple(np.array(gold["index"]).T)
     np.testing.assert_allclose(y[idx], gold["dwm32"], rtol=0, atol=1e-3)
     np.testing.assert_allclose(y[idx], gold["direct64"], rtol=0, atol=5e-3)
+
+
+@pytest.mark.parametrize("name", list(WORKLOADS))
+def test_baseline_workload_accuracy_default_engine(cuda, name):
+    """The engine bench.py runs (AUTO): MSE vs FP64 direct within the
+    reference's band and at or below the reference DWM's own MSE."""
+    wl = WORKLOADS[name]
+    desc = _native.make_desc(1, wl.c_in, wl.hw, wl.hw, wl.c_out, wl.spec().kernel, wl.spec().stride, wl.spec().pad)
+    engine = _native.ALGO_NAMES[_native.load().dwm_select_algo(desc, _native.DWM_F32, _native.DWM_ALGO_AUTO)]
+    d, g, spec, y = _run_workload(name, "auto", cuda)
+    m = mse(y, direct_conv2d_f64(d, g, spec))
+    gold = BASE[name]
+    assert m <= 1e-7
+    assert m <= MSE_TOL[engine] * gold["dwm32_mse"], (engine, m, gold["dwm32_mse"])
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["shape"][1] % 32 == 0 and c["f"] % 64 == 0],
+                         ids=lambda c: c["name"])
+def test_tc_engine_on_golden_cases(cuda, case):
+    d, g = ARR[f"{case['name']}/data"], ARR[f"{case['name']}/weights"]
+    spec = _spec(case)
+    y = dwm_conv2d(d, g, spec, precision="binary32", algo="tc")
+    ref32 = ARR[f"{case['name']}/dwm32"]
+    y64 = ARR[f"{case['name']}/direct64"]
+    assert mse(y, y64) <= mse(ref32, y64)
+    assert np.max(np.abs(y - ref32)) <= 4e-5 * max(1.0, np.max(np.abs(ref32)))
+
+
+@pytest.mark.parametrize("name", ["cfg4-3x3s1", "cfg4-7x7s1", "cfg4-11x11s1", "cfg5-5x5s2"])
+def test_tc_engine_batch_tail_and_determinism(cuda, name):
+    """A batch whose tile count is not a multiple of the 128-tile MMA block,
+    run twice: identical bytes, every image equal to that image alone."""
+    import torch
+    wl = WORKLOADS[name]
+    gen = torch.Generator(device=cuda).manual_seed(11)
+    x = torch.randn(3, wl.c_in, wl.hw, wl.hw, device=cuda, generator=gen)
+    w = torch.randn(wl.c_out, wl.c_in, wl.kernel, wl.kernel, device=cuda, generator=gen)
+    y1 = dwm_conv2d(x, w, wl.spec(), algo="tc")
+    y2 = dwm_conv2d(x, w, wl.spec(), algo="tc")
+    assert torch.equal(y1, y2)
+    y_one = dwm_conv2d(x[1:2].contiguous(), w, wl.spec(), algo="tc")
+    assert torch.equal(y_one[0], y1[1])
 
 
 def test_torch_tensor_io_and_counter(cuda):
