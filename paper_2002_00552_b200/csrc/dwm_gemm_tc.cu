@@ -17,21 +17,23 @@
 // chain into one accumulator is ~25x worse in MSE than the reference's RN FMA
 // chain.  Each 32-channel chunk therefore gets a fresh TMEM accumulator: its 8
 // small correction MMAs (hi*lo, lo*hi) go first, while the accumulator is
-// still small, then its 4 main MMAs (hi*hi); the epilogue sums the chunks in
-// FP32 round-to-nearest.  Emulated MSE vs the reference: 0.2-0.4x.
+// still small, then its main MMAs (hi*hi); the epilogue sums the chunks in
+// FP32 round-to-nearest.  Emulated MSE vs the reference: 0.2-0.4x.  (Chunks
+// are 16 channels, the granularity of the 4-deep TMEM A-operand ring.)
 //   Y_(i,j) += At_r[i][a] * At_c[j][b] * M_q     (coefficients 0, +-1)
 // and only y = interleave(Y) reaches HBM.
 //
 // Warp roles (320 threads, one CTA per SM, persistent over work items):
-//   warps 0-3  converter: V rows (one tile per thread) from HBM -> hi/lo ->
-//              tcgen05.st into a TMEM A-operand stage (double buffered)
+//   warps 0-3  converter: V row (one tile per thread) from the smem stage ->
+//              hi/lo -> tcgen05.st into a TMEM A-operand stage (double buffered)
 //   warps 4-7  epilogue : tcgen05.ld each chunk -> M_q (registers, FP32 RN);
 //              +-add M_q into the TMEM Y accumulators; at the end of a work
 //              item Y -> y (NCHW), non-finite flag
-//   warp 8     TMA producer for U_hi/U_lo tiles (SWIZZLE_128B, 4 stages)
+//   warp 8     TMA producer: V tile [128 tiles][32 ch] and U_hi/U_lo tiles
+//              [64 f][32 ch] per (frequency, chunk) stage (SWIZZLE_128B, 4 stages)
 //   warp 9     TMEM allocator + single-thread tcgen05.mma issuer (TS mode:
 //              A = V from TMEM, B = U from smem), commits to mbarriers
-// TMEM columns: chunk acc[2] 0-127, A stages 128-255 (hi 32 | lo 32 each), Y 256-511.
+// TMEM columns: chunk acc[2] 0-127, A stages 128-255 (4 x [hi 16 | lo 16]), Y 256-511.
 #include <cuda.h>
 #include <unistd.h>
 #include <cstdio>
@@ -50,21 +52,30 @@ constexpr int BM = 128;        // tiles per work item (MMA M, TMEM lanes)
 constexpr int BN = 64;         // filters per work item (MMA N)
 constexpr int BK = 32;         // channels per stage (128 B rows, one SW128 atom)
 constexpr int B_STAGES = 4;
-constexpr int A_STAGES = 2;
+#ifndef DWM_TC_AK
+#define DWM_TC_AK 32
+#endif
+constexpr int AK = DWM_TC_AK;       // channels per A stage / per accumulator chunk
+constexpr int A_STAGES = 64 / AK;   // TMEM A-operand ring in 128 columns (hi AK | lo AK each)
 constexpr int THREADS = 320;
 constexpr int MAX_FREQS = 1024;
 constexpr uint32_t U_TILE_BYTES = BN * BK * 4;  // 8 KB per plane
+constexpr uint32_t V_TILE_BYTES = BM * BK * 4;  // 16 KB
 constexpr uint32_t COL_ACC = 0, COL_A = 128, COL_Y = 256;
 
 // Debug builds (-DDWM_TC_TRACE) publish per-role progress into mapped host
 // memory so a stuck pipeline can be diagnosed while the kernel still runs.
 #ifdef DWM_TC_TRACE
 #define TRACE(slot, val) do { if (trace) { trace[slot] = (val); __threadfence_system(); } } while (0)
+// per-role cycles spent blocked in mbarrier waits (block 0, one thread per role)
+#define TWAIT(acc, bar, ph) do { long long _t0 = clock64(); mbar_wait(bar, ph); acc += clock64() - _t0; } while (0)
 #else
 #define TRACE(slot, val) do { } while (0)
+#define TWAIT(acc, bar, ph) mbar_wait(bar, ph)
 #endif
 
 struct __align__(1024) Smem {
+  float v[B_STAGES][BM * BK];
   float u_hi[B_STAGES][BN * BK];
   float u_lo[B_STAGES][BN * BK];
   uint64_t b_full[B_STAGES], b_empty[B_STAGES];
@@ -81,7 +92,7 @@ __device__ __forceinline__ int at_coef_rt(int r, int i, int a) {
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_constant__ CUtensorMap map_uhi,
+gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_uhi,
                const __grid_constant__ CUtensorMap map_ulo, float* __restrict__ y, int32_t* __restrict__ flag,
                volatile int* trace) {
   extern __shared__ uint8_t smem_raw[];
@@ -97,7 +108,7 @@ gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_con
   if (tid == 0) {
     for (int i = 0; i < B_STAGES; ++i) {
       mbar_init(&S.b_full[i], 1);
-      mbar_init(&S.b_empty[i], 1);
+      mbar_init(&S.b_empty[i], 1 + 4);  // MMA commit (U) + 4 converter warps (V)
     }
     for (int i = 0; i < A_STAGES; ++i) {
       mbar_init(&S.a_full[i], 4);
@@ -120,6 +131,7 @@ gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_con
       }
   }
   if (warp == 8 && lane == 0) {
+    tma_prefetch_desc(&map_v);
     tma_prefetch_desc(&map_uhi);
     tma_prefetch_desc(&map_ulo);
   }
@@ -129,102 +141,111 @@ gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_con
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
   if (tid == 0 && blockIdx.x == 0) TRACE(0, 1);
+#ifdef DWM_TC_TRACE
+  long long w_tma = 0, w_mma_b = 0, w_mma_acc = 0, w_mma_a = 0, w_cv_b = 0, w_cv_a = 0, w_ep = 0;
+  const long long t_start = clock64();
+#endif
 
   if (warp == 8) {
-    // ================= TMA producer: U_hi / U_lo tiles =================
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-        const int n0 = (int)(w % n_nblk) * BN;
-        for (int q = 0; q < Q; ++q)
-          for (int kc = 0; kc < KC; ++kc, ++it) {
-            const uint32_t s = it % B_STAGES, round = it / B_STAGES;
-            if (blockIdx.x == 0) TRACE(1, (int)it);
-            mbar_wait(&S.b_empty[s], (round & 1) ^ 1);
-            mbar_arrive_expect_tx(&S.b_full[s], 2 * U_TILE_BYTES);
+    // ================= TMA producer (whole warp converged, one lane issues) =================
+    uint32_t it = 0;
+    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const int n0 = (int)(w % n_nblk) * BN;
+      const int m0 = (int)(w / n_nblk) * BM;
+      for (int q = 0; q < Q; ++q)
+        for (int kc = 0; kc < KC; ++kc, ++it) {
+          const uint32_t s = it % B_STAGES, round = it / B_STAGES;
+          TWAIT(w_tma, &S.b_empty[s], (round & 1) ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&S.b_full[s], V_TILE_BYTES + 2 * U_TILE_BYTES);
+            tma_load_3d(S.v[s], &map_v, &S.b_full[s], kc * BK, m0, q);
             tma_load_2d(S.u_hi[s], &map_uhi, &S.b_full[s], kc * BK, q * F + n0);
             tma_load_2d(S.u_lo[s], &map_ulo, &S.b_full[s], kc * BK, q * F + n0);
           }
-      }
+          __syncwarp();
+        }
     }
-    __syncwarp();  // keep the warp converged before the final block barrier
   } else if (warp == 9) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
+    // ================= MMA issuer (whole warp converged, one lane issues) =================
+    {
       const uint32_t idesc = idesc_tf32(BM, BN);
       uint32_t itb = 0, ita = 0;
       for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
         for (int q = 0; q < Q; ++q) {
-          for (int kc = 0; kc < KC; ++kc, ++itb, ++ita) {
-            // one fresh accumulator per 32-channel chunk (ring of 2)
-            const uint32_t ab = ita % 2;
-            const uint32_t dacc = tmem + COL_ACC + ab * BN;
-            if (blockIdx.x == 0) TRACE(2, (int)(ita * 10 + 1));
-            mbar_wait(&S.acc_empty[ab], ((ita / 2) & 1) ^ 1);
-            const uint32_t sb = itb % B_STAGES, sa = ita % A_STAGES;
-            if (blockIdx.x == 0) TRACE(3, (int)(ita * 10 + 2));
-            mbar_wait(&S.a_full[sa], (ita / A_STAGES) & 1);
-            if (blockIdx.x == 0) TRACE(3, (int)(ita * 10 + 3));
-            mbar_wait(&S.b_full[sb], (itb / B_STAGES) & 1);
-            if (blockIdx.x == 0) TRACE(3, (int)(ita * 10 + 4));
-            tc_fence_after();
-            const uint32_t a_hi = tmem + COL_A + sa * 64, a_lo = a_hi + 32;
-            const uint32_t bh = smem_u32(S.u_hi[sb]), bl = smem_u32(S.u_lo[sb]);
-            // small correction products first, while the accumulator is small
+          for (int kc = 0; kc < KC; ++kc, ++itb) {
+            const uint32_t sb = itb % B_STAGES;
+            TWAIT(w_mma_b, &S.b_full[sb], (itb / B_STAGES) & 1);
+            const uint64_t dh0 = sdesc_sw128(smem_u32(S.u_hi[sb])), dl0 = sdesc_sw128(smem_u32(S.u_lo[sb]));
 #pragma unroll
-            for (int k = 0; k < BK / 8; ++k) {
-              mma_tf32_ts(dacc, a_hi + 8 * k, sdesc_sw128(bl + 32 * k), idesc, k != 0);
-              mma_tf32_ts(dacc, a_lo + 8 * k, sdesc_sw128(bh + 32 * k), idesc, 1);
+            for (int h = 0; h < BK / AK; ++h, ++ita) {
+              // one fresh accumulator per AK-channel chunk (ring of 2)
+              const uint32_t ab = ita % 2, sa = ita % A_STAGES;
+              const uint32_t dacc = tmem + COL_ACC + ab * BN;
+              TWAIT(w_mma_acc, &S.acc_empty[ab], ((ita / 2) & 1) ^ 1);
+              TWAIT(w_mma_a, &S.a_full[sa], (ita / A_STAGES) & 1);
+              tc_fence_after();
+              const uint32_t a_hi = tmem + COL_A + sa * (2 * AK), a_lo = a_hi + AK;
+              if (elect_one()) {
+                // small correction products first, while the accumulator is small
+#pragma unroll
+                for (int k = 0; k < AK / 8; ++k) {
+                  const uint32_t kd = 2 * (h * (AK / 8) + k);  // +32 B per K=8 slice, in 16-byte descriptor units
+                  mma_tf32_ts(dacc, a_hi + 8 * k, dl0 + kd, idesc, k != 0);
+                  mma_tf32_ts(dacc, a_lo + 8 * k, dh0 + kd, idesc, 1);
+                }
+#pragma unroll
+                for (int k = 0; k < AK / 8; ++k) mma_tf32_ts(dacc, a_hi + 8 * k, dh0 + 2 * (h * (AK / 8) + k), idesc, 1);
+                mma_commit(&S.a_empty[sa]);
+                mma_commit(&S.acc_full[ab]);
+              }
+              __syncwarp();
             }
-#pragma unroll
-            for (int k = 0; k < BK / 8; ++k) mma_tf32_ts(dacc, a_hi + 8 * k, sdesc_sw128(bh + 32 * k), idesc, 1);
-            mma_commit(&S.a_empty[sa]);
-            mma_commit(&S.b_empty[sb]);
-            mma_commit(&S.acc_full[ab]);
+            if (elect_one()) mma_commit(&S.b_empty[sb]);
+            __syncwarp();
           }
         }
       }
     }
-    __syncwarp();
   } else if (warp < 4) {
-    // ================= converter: V -> hi/lo -> TMEM A stage =================
+    // ================= converter: V stage (smem) -> hi/lo -> TMEM A stage =================
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * warp) << 16);
     const int m = 32 * warp + lane;
-    uint32_t ita = 0;
+    uint32_t ita = 0, ita2 = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-      const int64_t tile = (w / n_nblk) * BM + m;
-      const bool live = tile < d.tiles;
       for (int q = 0; q < Q; ++q) {
-        const float* row = V + ((size_t)q * d.tiles + (live ? tile : 0)) * C;
         for (int kc = 0; kc < KC; ++kc, ++ita) {
+          const uint32_t sb = ita % B_STAGES;
+          TWAIT(w_cv_b, &S.b_full[sb], (ita / B_STAGES) & 1);
           float hi[32], lo[32];
-          const float4* src = reinterpret_cast<const float4*>(row + kc * BK);
+          const uint8_t* vrow = reinterpret_cast<const uint8_t*>(S.v[sb]);
 #pragma unroll
-          for (int v4 = 0; v4 < 8; ++v4) {
-            float4 x = live ? __ldg(src + v4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int c4 = 0; c4 < 8; ++c4) {
+            // row m, 16-byte chunk c4 of the SWIZZLE_128B tile
+            const float4 x = *reinterpret_cast<const float4*>(vrow + sw128_offset(m, 4 * c4));
             const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float h = tf32_rn(xs[e]);
-              hi[v4 * 4 + e] = h;
-              lo[v4 * 4 + e] = tf32_rn(xs[e] - h);
+              hi[c4 * 4 + e] = h;
+              lo[c4 * 4 + e] = tf32_rn(xs[e] - h);
             }
           }
-          const uint32_t sa = ita % A_STAGES;
-          if (blockIdx.x == 0 && tid == 0) TRACE(4, (int)(ita * 10 + 1));
-          mbar_wait(&S.a_empty[sa], ((ita / A_STAGES) & 1) ^ 1);
-          if (blockIdx.x == 0 && tid == 0) TRACE(4, (int)(ita * 10 + 2));
-          tc_fence_after();
-          const uint32_t base = lane_addr + COL_A + sa * 64;
-          tmem_st16(base + 0, *reinterpret_cast<float(*)[16]>(hi));
-          tmem_st16(base + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
-          tmem_st16(base + 32, *reinterpret_cast<float(*)[16]>(lo));
-          tmem_st16(base + 48, *reinterpret_cast<float(*)[16]>(lo + 16));
-          tmem_st_wait();
-          tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&S.a_full[sa]);
-          if (blockIdx.x == 0 && tid == 0) TRACE(4, (int)(ita * 10 + 3));
+          if (lane == 0) mbar_arrive(&S.b_empty[sb]);  // this warp is done with the V rows
+#pragma unroll
+          for (int h = 0; h < BK / AK; ++h) {
+            const uint32_t sa = ita2 % A_STAGES;
+            TWAIT(w_cv_a, &S.a_empty[sa], ((ita2 / A_STAGES) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t base = lane_addr + COL_A + sa * (2 * AK);
+            tmem_st16(base, *reinterpret_cast<float(*)[16]>(hi + h * AK));
+            tmem_st16(base + AK, *reinterpret_cast<float(*)[16]>(lo + h * AK));
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.a_full[sa]);
+            ++ita2;
+          }
         }
       }
     }
@@ -248,10 +269,9 @@ gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_con
       }
       for (int q = 0; q < Q; ++q) {
         float mq[BN];
-        for (int kc = 0; kc < KC; ++kc, ++itq) {
+        for (int kc = 0; kc < KC * (BK / AK); ++kc, ++itq) {
           const uint32_t ab = itq % 2;
-          if (blockIdx.x == 0 && tid == 128) TRACE(5, (int)(itq * 10 + 1));
-          mbar_wait(&S.acc_full[ab], (itq / 2) & 1);
+          TWAIT(w_ep, &S.acc_full[ab], (itq / 2) & 1);
           tc_fence_after();
           float part[BN];
 #pragma unroll
@@ -269,7 +289,6 @@ gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_con
             for (int j = 0; j < BN; ++j) mq[j] = __fadd_rn(mq[j], part[j]);
           }
         }
-        if (blockIdx.x == 0 && tid == 128) TRACE(5, (int)(itq * 10 + 2));
         // output transform: Y_p +-= M_q for the positions p with a nonzero coefficient
         const int8_t cf[4] = {S.coef[q][0], S.coef[q][1], S.coef[q][2], S.coef[q][3]};
 #pragma unroll
@@ -291,7 +310,6 @@ gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_con
           for (int ch = 0; ch < BN; ch += 16) tmem_st16(ya + ch, *reinterpret_cast<float(*)[16]>(yv + ch));
         }
         tmem_st_wait();
-        if (blockIdx.x == 0 && tid == 128) TRACE(5, (int)(itq * 10 + 3));
       }
       // Y -> y: positions (i, j) of tile (n, ty, tx), filters n0..n0+BN.
       // tcgen05.ld is warp-collective: every lane loads, only live tiles store.
@@ -342,6 +360,15 @@ gemm_tc_kernel(const dwm_desc_t d, const float* __restrict__ V, const __grid_con
   }
 
   if (blockIdx.x == 0 && lane == 0) TRACE(8 + warp, 1);
+#ifdef DWM_TC_TRACE
+  if (blockIdx.x == 0) {
+    const long long tot = clock64() - t_start;
+    if (tid == 0) { TRACE(20, (int)(tot >> 10)); TRACE(21, (int)(w_cv_b >> 10)); TRACE(22, (int)(w_cv_a >> 10)); }
+    if (tid == 128) TRACE(23, (int)(w_ep >> 10));
+    if (tid == 256) TRACE(24, (int)(w_tma >> 10));
+    if (tid == 288) { TRACE(25, (int)(w_mma_b >> 10)); TRACE(26, (int)(w_mma_acc >> 10)); TRACE(27, (int)(w_mma_a >> 10)); }
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tmem);
@@ -357,6 +384,21 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
       fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
   }
   return fn;
+}
+
+int make_v_map(CUtensorMap* map, const float* base, const dwm_desc_t& d) {
+  auto encode = get_encode();
+  if (!encode) return fail(DWM_ECUDA, "cuTensorMapEncodeTiled is unavailable");
+  // [freq][tiles][C]: rows past `tiles` of a frequency read as zeros
+  const cuuint64_t dims[3] = {(cuuint64_t)d.c, (cuuint64_t)d.tiles, (cuuint64_t)d.num_freqs};
+  const cuuint64_t strides[2] = {(cuuint64_t)d.c * sizeof(float), (cuuint64_t)d.tiles * d.c * sizeof(float)};
+  const cuuint32_t box[3] = {BK, BM, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DWM_ECUDA, "cuTensorMapEncodeTiled(V) failed (%d)", (int)r);
+  return DWM_OK;
 }
 
 int make_u_map(CUtensorMap* map, const float* base, const dwm_desc_t& d) {
@@ -376,14 +418,15 @@ int make_u_map(CUtensorMap* map, const float* base, const dwm_desc_t& d) {
 }  // namespace
 
 bool tc_gemm_supported(const dwm_desc_t& d) {
-  return d.c % BK == 0 && d.f % BN == 0 && d.num_freqs <= MAX_FREQS && ((uint64_t)d.c * 4) % 16 == 0;
+  return d.c % BK == 0 && d.f % BN == 0 && d.num_freqs <= MAX_FREQS && d.tiles < ((int64_t)1 << 31);
 }
 
 int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag, cudaStream_t s) {
   if (!tc_gemm_supported(d)) return fail(DWM_EUNSUPPORTED, "tcgen05 GEMM needs C %% 32 == 0 and F %% 64 == 0");
   const float* uhi = (const float*)U;
   const float* ulo = uhi + (size_t)d.num_freqs * d.f * d.c;
-  CUtensorMap mh, ml;
+  CUtensorMap mv, mh, ml;
+  if (int st = make_v_map(&mv, (const float*)V, d)) return st;
   if (int st = make_u_map(&mh, uhi, d)) return st;
   if (int st = make_u_map(&ml, ulo, d)) return st;
   const size_t smem = sizeof(Smem) + 1024;
@@ -399,15 +442,17 @@ int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, i
   if (!trace_h) DWM_CUDA_TRY(cudaHostAlloc((void**)&trace_h, 64 * sizeof(int), cudaHostAllocMapped));
   for (int i = 0; i < 64; ++i) trace_h[i] = -1;
   DWM_CUDA_TRY(cudaHostGetDevicePointer((void**)&trace_d, trace_h, 0));
-  gemm_tc_kernel<<<grid, THREADS, smem, s>>>(d, (const float*)V, mh, ml, (float*)y, flag, trace_d);
+  gemm_tc_kernel<<<grid, THREADS, smem, s>>>(d, mv, mh, ml, (float*)y, flag, trace_d);
   DWM_CUDA_TRY(cudaGetLastError());
   for (int i = 0; i < 50 && cudaStreamQuery(s) == cudaErrorNotReady; ++i) usleep(100000);
   fprintf(stderr, "[tc trace] done=%d setup=%d tma_it=%d mma_q=%d mma_kc=%d conv=%d epi=%d exits:", 
           cudaStreamQuery(s) == cudaSuccess, trace_h[0], trace_h[1], trace_h[2], trace_h[3], trace_h[4], trace_h[5]);
   for (int w = 0; w < 10; ++w) fprintf(stderr, " %d", trace_h[8 + w]);
-  fprintf(stderr, "\n");
+  fprintf(stderr, "\n[tc trace] kcycles total %d | conv wait V %d wait A-slot %d | epi wait acc %d | tma wait slot %d | "
+          "mma wait U %d wait acc-slot %d wait A %d\n", trace_h[20], trace_h[21], trace_h[22], trace_h[23], trace_h[24],
+          trace_h[25], trace_h[26], trace_h[27]);
 #else
-  gemm_tc_kernel<<<grid, THREADS, smem, s>>>(d, (const float*)V, mh, ml, (float*)y, flag, nullptr);
+  gemm_tc_kernel<<<grid, THREADS, smem, s>>>(d, mv, mh, ml, (float*)y, flag, nullptr);
   DWM_CUDA_TRY(cudaGetLastError());
 #endif
   return DWM_OK;

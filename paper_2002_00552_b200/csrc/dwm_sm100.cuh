@@ -55,8 +55,8 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   if (mbar_try_wait(bar, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait(bar, phase)) {
-    if (globaltimer_ns() - t0 > 2000000000ull) {
+  for (uint32_t polls = 1; !mbar_try_wait(bar, phase); ++polls) {
+    if ((polls & 1023u) == 0 && globaltimer_ns() - t0 > 2000000000ull) {
       printf("dwm: mbarrier wait timeout (block %d thread %d phase %u)\n", blockIdx.x, threadIdx.x, phase);
       __trap();
     }
@@ -81,6 +81,16 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* desc, ui
           smem_u32(smem_dst)),
       "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// One lane of a converged warp (elect.sync).  Issuing tcgen05/TMA from a
+// converged warp lets ptxas keep the operands in uniform registers; issuing
+// from a lane-divergent branch costs an R2UR/ELECT loop per instruction and
+// measured 2-4x lower MMA issue rate (tools/commit_probe.cu).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
 }
 
 // ------------------------------------------------------------------ tcgen05

@@ -182,6 +182,100 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Input transform, shared-memory staged: one CTA per (image, tile row,
+// 32-channel block).  The r_h + s_h padded-input rows that tile row reads are
+// staged once in shared memory with coalesced row loads; each warp then owns
+// tiles, each lane one channel, so every V store is a coalesced 128-byte row
+// segment of V[fq][tile][c].  Same arithmetic (and bits) as the kernel above.
+// ---------------------------------------------------------------------------
+constexpr int IT_CB = 32;  // channels per CTA (one per lane)
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged) {
+  extern __shared__ __align__(16) unsigned char it_smem_raw[];
+  T* sx = reinterpret_cast<T*>(it_smem_raw);  // [IT_CB][rows_staged][W] with odd channel pitch
+  const int pitch = rows_staged * d.w + 1;
+  const int ty = blockIdx.x % d.th;
+  const int n = blockIdx.x / d.th;
+  const int c0 = blockIdx.y * IT_CB;
+  const int cb = min(IT_CB, d.c - c0);
+  const int row0 = 2 * ty * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
+
+  // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
+  for (int cc = threadIdx.x / 32; cc < cb; cc += blockDim.x / 32) {
+    const T* xc = x + ((int64_t)n * d.c + c0 + cc) * d.h * d.w;
+    for (int e = threadIdx.x % 32; e < rows_staged * d.w; e += 32) {
+      const int r = e / d.w, col = e % d.w;
+      const int row = row0 + r;
+      sx[cc * pitch + e] = (row >= 0 && row < d.h) ? __ldg(xc + (int64_t)row * d.w + col) : T(0);
+    }
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nwarps = blockDim.x / 32;
+  if (lane >= cb) return;
+  const T* sc = sx + lane * pitch;
+  const int64_t tc_stride = d.tiles * d.c;
+  for (int tx = warp; tx < d.tw; tx += nwarps) {
+    const int64_t tile = ((int64_t)n * d.th + ty) * d.tw + tx;
+    T* vout = V + tile * d.c + c0 + lane;
+    int fq = 0;
+    for (int rp = 0; rp < d.n_row_parts; ++rp) {
+      const dwm_axis_part_t R = d.row_parts[rp];
+      const int pr = R.count, lr = pr + 1;
+      int rows[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = 2 * ty + i;
+        const int rs = R.origin + d.s_h * i;  // staged-row index
+        const int row = row0 + rs;
+        rows[i] = (i < lr && k < d.oh - 1 + pr && row >= 0 && row < d.h) ? rs * d.w : -1;
+      }
+      for (int cp = 0; cp < d.n_col_parts; ++cp) {
+        const dwm_axis_part_t Cc = d.col_parts[cp];
+        const int pc = Cc.count, lc = pc + 1;
+        int cols[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = 2 * tx + j;
+          const int col = Cc.origin + d.s_w * k - d.pad_left;
+          cols[j] = (j < lc && k < d.ow - 1 + pc && col >= 0 && col < d.w) ? col : -1;
+        }
+        T win[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? sc[rows[i] + cols[j]] : T(0);
+        T t[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            T acc = mul_rn((T)c_bt[pr][a][0], win[0][j]);
+#pragma unroll
+            for (int i = 1; i < 4; ++i)
+              if (i < lr) acc = fma_rn((T)c_bt[pr][a][i], win[i][j], acc);
+            t[a][j] = acc;
+          }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (a < lr && b < lc) {
+              T acc = mul_rn(t[a][0], (T)c_bt[pc][b][0]);
+#pragma unroll
+              for (int j = 1; j < 4; ++j)
+                if (j < lc) acc = fma_rn(t[a][j], (T)c_bt[pc][b][j], acc);
+              vout[(int64_t)(fq + a * lc + b) * tc_stride] = acc;
+            }
+        fq += lr * lc;
+      }
+    }
+  }
+}
+
 static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s) {
@@ -201,7 +295,29 @@ int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* 
   return DWM_OK;
 }
 
+template <typename T>
+static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaStream_t s, bool* used) {
+  // rows a tile row reads: (largest tap origin + s*count) over row parts = r_h + s_h - 1, +1
+  int rows = 0;
+  for (int i = 0; i < d.n_row_parts; ++i)
+    rows = max(rows, d.row_parts[i].origin + d.s_h * d.row_parts[i].count + 1);
+  const size_t smem = (size_t)IT_CB * ((size_t)rows * d.w + 1) * sizeof(T);
+  *used = false;
+  if (smem > 96 * 1024 || d.c < 8) return DWM_OK;
+  DWM_CUDA_TRY(cudaFuncSetAttribute(input_transform_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  const dim3 grid((unsigned)((int64_t)d.n * d.th), (unsigned)((d.c + IT_CB - 1) / IT_CB));
+  input_transform_smem_kernel<T><<<grid, 256, smem, s>>>(d, (const T*)x, (T*)V, rows);
+  DWM_CUDA_TRY(cudaGetLastError());
+  *used = true;
+  return DWM_OK;
+}
+
 int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s) {
+  bool used = false;
+  const int st = dtype == DWM_F64 ? launch_input_smem<double>(d, x, V, s, &used)
+                                  : launch_input_smem<float>(d, x, V, s, &used);
+  if (st || used) return st;
   const int64_t n = d.tiles * d.c;
   if (dtype == DWM_F64)
     input_transform_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(d, (const double*)x, (double*)V);

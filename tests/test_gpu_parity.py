@@ -103,7 +103,7 @@ def test_baseline_workload_accuracy_exact(cuda, name):
     gold = BASE[name]
     m = mse(y, y64)
     assert m <= 1e-7
-    assert m <= MSE_TOL["exact"] * gold["dwm32_mse"], (m, gold["dwm32_mse"])
+    assert m <= MSE_TOL["exact"] * gold["dwm32_mse"] * (1 + 1e-9), (m, gold["dwm32_mse"])
     idx = tuple(np.array(gold["index"]).T)
     np.testing.assert_allclose(y[idx], gold["dwm32"], rtol=0, atol=1e-3)
     np.testing.assert_allclose(y[idx], gold["direct64"], rtol=0, atol=5e-3)
@@ -120,7 +120,8 @@ def test_baseline_workload_accuracy_default_engine(cuda, name):
     m = mse(y, direct_conv2d_f64(d, g, spec))
     gold = BASE[name]
     assert m <= 1e-7
-    assert m <= MSE_TOL[engine] * gold["dwm32_mse"], (engine, m, gold["dwm32_mse"])
+    # (1 + 1e-9): the FP64 ground truth is recomputed here with another summation order
+    assert m <= MSE_TOL[engine] * gold["dwm32_mse"] * (1 + 1e-9), (engine, m, gold["dwm32_mse"])
 
 
 @pytest.mark.parametrize("case", [c for c in CASES if c["shape"][1] % 32 == 0 and c["f"] % 64 == 0],
