@@ -23,16 +23,18 @@
 //   Y_(i,j) += At_r[i][a] * At_c[j][b] * M_q     (coefficients 0, +-1)
 // and only y = interleave(Y) reaches HBM.
 //
-// Warp roles (320 threads, one CTA per SM, persistent over work items):
+// Warp roles (448 threads, one CTA per SM, persistent over work items):
 //   warps 0-3  converter: V row (one tile per thread) from the smem stage ->
 //              hi/lo -> tcgen05.st into a TMEM A-operand stage (double buffered)
-//   warps 4-7  epilogue : tcgen05.ld each chunk -> M_q (registers, FP32 RN);
+//   warps 4-11 epilogue : tcgen05.ld each chunk -> M_q (registers, FP32 RN);
 //              +-add M_q into the TMEM Y accumulators; at the end of a work
-//              item Y -> y (NCHW), non-finite flag
-//   warp 8     TMA producer: V tile [128 tiles][32 ch] and U_hi/U_lo tiles
-//              [64 f][32 ch] per (frequency, chunk) stage (SWIZZLE_128B, 4 stages)
-//   warp 9     TMEM allocator + single-thread tcgen05.mma issuer (TS mode:
-//              A = V from TMEM, B = U from smem), commits to mbarriers
+//              item Y -> y (NCHW), non-finite flag.  Two warps per TMEM lane
+//              quadrant, 32 filter columns each.
+//   warp 12    TMA producer: V tile [128 tiles][32 ch] and U_hi/U_lo tiles
+//              [64 f][32 ch] per (frequency, chunk) stage (SWIZZLE_128B, 6 stages)
+//   warp 13    TMEM allocator + tcgen05.mma issuer (TS mode: A = V from TMEM,
+//              B = U from smem), commits to mbarriers; issue from the
+//              converged warp via elect.sync
 // TMEM columns: chunk acc[2] 0-127, A stages 128-255 (4 x [hi 16 | lo 16]), Y 256-511.
 #include <cuda.h>
 #include <unistd.h>
@@ -51,13 +53,16 @@ using namespace sm100;
 constexpr int BM = 128;        // tiles per work item (MMA M, TMEM lanes)
 constexpr int BN = 64;         // filters per work item (MMA N)
 constexpr int BK = 32;         // channels per stage (128 B rows, one SW128 atom)
-constexpr int B_STAGES = 4;
+constexpr int B_STAGES = 6;
 #ifndef DWM_TC_AK
 #define DWM_TC_AK 32
 #endif
 constexpr int AK = DWM_TC_AK;       // channels per A stage / per accumulator chunk
 constexpr int A_STAGES = 64 / AK;   // TMEM A-operand ring in 128 columns (hi AK | lo AK each)
-constexpr int THREADS = 320;
+constexpr int THREADS = 448;    // 4 converter + 8 epilogue + TMA + MMA warps
+constexpr int EPI_WARPS = 8;
+constexpr int EC = BN / (EPI_WARPS / 4);  // columns per epilogue warp (32)
+constexpr int WARP_TMA = 12, WARP_MMA = 13;
 constexpr int MAX_FREQS = 1024;
 constexpr uint32_t U_TILE_BYTES = BN * BK * 4;  // 8 KB per plane
 constexpr uint32_t V_TILE_BYTES = BM * BK * 4;  // 16 KB
@@ -116,7 +121,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.acc_full[i], 1);
-      mbar_init(&S.acc_empty[i], 4);
+      mbar_init(&S.acc_empty[i], EPI_WARPS);
     }
     fence_barrier_init();
     // output-transform coefficient of every frequency for the 4 tile positions
@@ -130,12 +135,12 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
               for (int j = 0; j < 2; ++j) S.coef[q][i * 2 + j] = (int8_t)(at_coef_rt(pr, i, a) * at_coef_rt(pc, j, b));
       }
   }
-  if (warp == 8 && lane == 0) {
+  if (warp == WARP_TMA && lane == 0) {
     tma_prefetch_desc(&map_v);
     tma_prefetch_desc(&map_uhi);
     tma_prefetch_desc(&map_ulo);
   }
-  if (warp == 9) tmem_alloc<512>(&S.tmem_base);
+  if (warp == WARP_MMA) tmem_alloc<512>(&S.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -146,7 +151,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
   const long long t_start = clock64();
 #endif
 
-  if (warp == 8) {
+  if (warp == WARP_TMA) {
     // ================= TMA producer (whole warp converged, one lane issues) =================
     uint32_t it = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
@@ -165,7 +170,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           __syncwarp();
         }
     }
-  } else if (warp == 9) {
+  } else if (warp == WARP_MMA) {
     // ================= MMA issuer (whole warp converged, one lane issues) =================
     {
       const uint32_t idesc = idesc_tf32(BM, BN);
@@ -174,7 +179,8 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         for (int q = 0; q < Q; ++q) {
           for (int kc = 0; kc < KC; ++kc, ++itb) {
             const uint32_t sb = itb % B_STAGES;
-            TWAIT(w_mma_b, &S.b_full[sb], (itb / B_STAGES) & 1);
+            // no b_full wait: the converter only signals a_full after it
+            // observed b_full, and the same TMA transaction carried the U tiles
             const uint64_t dh0 = sdesc_sw128(smem_u32(S.u_hi[sb])), dl0 = sdesc_sw128(smem_u32(S.u_lo[sb]));
 #pragma unroll
             for (int h = 0; h < BK / AK; ++h, ++ita) {
@@ -238,8 +244,11 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             TWAIT(w_cv_a, &S.a_empty[sa], ((ita2 / A_STAGES) & 1) ^ 1);
             tc_fence_after();
             const uint32_t base = lane_addr + COL_A + sa * (2 * AK);
-            tmem_st16(base, *reinterpret_cast<float(*)[16]>(hi + h * AK));
-            tmem_st16(base + AK, *reinterpret_cast<float(*)[16]>(lo + h * AK));
+#pragma unroll
+            for (int c = 0; c < AK; c += 16) {
+              tmem_st16(base + c, *reinterpret_cast<float(*)[16]>(hi + h * AK + c));
+              tmem_st16(base + AK + c, *reinterpret_cast<float(*)[16]>(lo + h * AK + c));
+            }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -251,42 +260,46 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     }
   } else {
     // ================= epilogue: M_q -> Y (TMEM) -> y =================
-    const int ew = warp - 4;  // lane quadrant
-    const uint32_t lane_addr = tmem + ((uint32_t)(32 * ew) << 16);
-    const int m = 32 * ew + lane;
+    // 8 warps: TMEM lane quadrant = warp % 4 (hardware rule), column half = (warp - 4) / 4
+    const int quad = warp % 4;
+    const int c0 = ((warp - 4) / 4) * EC;
+    const uint32_t lane_addr = tmem + ((uint32_t)(32 * quad) << 16);
+    const int m = 32 * quad + lane;
     uint32_t itq = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
       const int64_t tile = (w / n_nblk) * BM + m;
       const int n0 = (int)(w % n_nblk) * BN;
-      // zero the Y accumulators of this lane
+      // zero this warp's Y accumulators
       {
         float z[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) z[j] = 0.f;
 #pragma unroll
-        for (int c = 0; c < 4 * BN; c += 16) tmem_st16(lane_addr + COL_Y + c, z);
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int c = 0; c < EC; c += 16) tmem_st16(lane_addr + COL_Y + p * BN + c0 + c, z);
         tmem_st_wait();
       }
       for (int q = 0; q < Q; ++q) {
-        float mq[BN];
+        float mq[EC];
         for (int kc = 0; kc < KC * (BK / AK); ++kc, ++itq) {
           const uint32_t ab = itq % 2;
           TWAIT(w_ep, &S.acc_full[ab], (itq / 2) & 1);
           tc_fence_after();
-          float part[BN];
+          float part[EC];
 #pragma unroll
-          for (int ch = 0; ch < BN; ch += 16)
-            tmem_ld16(lane_addr + COL_ACC + ab * BN + ch, *reinterpret_cast<float(*)[16]>(part + ch));
+          for (int ch = 0; ch < EC; ch += 16)
+            tmem_ld16(lane_addr + COL_ACC + ab * BN + c0 + ch, *reinterpret_cast<float(*)[16]>(part + ch));
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&S.acc_empty[ab]);
           if (kc == 0) {
 #pragma unroll
-            for (int j = 0; j < BN; ++j) mq[j] = part[j];
+            for (int j = 0; j < EC; ++j) mq[j] = part[j];
           } else {
 #pragma unroll
-            for (int j = 0; j < BN; ++j) mq[j] = __fadd_rn(mq[j], part[j]);
+            for (int j = 0; j < EC; ++j) mq[j] = __fadd_rn(mq[j], part[j]);
           }
         }
         // output transform: Y_p +-= M_q for the positions p with a nonzero coefficient
@@ -294,24 +307,24 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
           if (cf[p] == 0) continue;
-          float yv[BN];
-          const uint32_t ya = lane_addr + COL_Y + p * BN;
+          float yv[EC];
+          const uint32_t ya = lane_addr + COL_Y + p * BN + c0;
 #pragma unroll
-          for (int ch = 0; ch < BN; ch += 16) tmem_ld16(ya + ch, *reinterpret_cast<float(*)[16]>(yv + ch));
+          for (int ch = 0; ch < EC; ch += 16) tmem_ld16(ya + ch, *reinterpret_cast<float(*)[16]>(yv + ch));
           tmem_ld_wait();
           if (cf[p] > 0) {
 #pragma unroll
-            for (int j = 0; j < BN; ++j) yv[j] = __fadd_rn(yv[j], mq[j]);
+            for (int j = 0; j < EC; ++j) yv[j] = __fadd_rn(yv[j], mq[j]);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN; ++j) yv[j] = __fsub_rn(yv[j], mq[j]);
+            for (int j = 0; j < EC; ++j) yv[j] = __fsub_rn(yv[j], mq[j]);
           }
 #pragma unroll
-          for (int ch = 0; ch < BN; ch += 16) tmem_st16(ya + ch, *reinterpret_cast<float(*)[16]>(yv + ch));
+          for (int ch = 0; ch < EC; ch += 16) tmem_st16(ya + ch, *reinterpret_cast<float(*)[16]>(yv + ch));
         }
         tmem_st_wait();
       }
-      // Y -> y: positions (i, j) of tile (n, ty, tx), filters n0..n0+BN.
+      // Y -> y: positions (i, j) of tile (n, ty, tx), this warp's filters.
       // tcgen05.ld is warp-collective: every lane loads, only live tiles store.
       {
         const bool live = tile < d.tiles;
@@ -322,16 +335,16 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         const int n = (int)(t2 / d.th);
         bool bad = false;
 #pragma unroll 1
-        for (int ch = 0; ch < BN; ch += 16) {
+        for (int ch = 0; ch < EC; ch += 16) {
           float y00[16], y01[16], y10[16], y11[16];
-          tmem_ld16(lane_addr + COL_Y + 0 * BN + ch, y00);
-          tmem_ld16(lane_addr + COL_Y + 1 * BN + ch, y01);
-          tmem_ld16(lane_addr + COL_Y + 2 * BN + ch, y10);
-          tmem_ld16(lane_addr + COL_Y + 3 * BN + ch, y11);
+          tmem_ld16(lane_addr + COL_Y + 0 * BN + c0 + ch, y00);
+          tmem_ld16(lane_addr + COL_Y + 1 * BN + c0 + ch, y01);
+          tmem_ld16(lane_addr + COL_Y + 2 * BN + c0 + ch, y10);
+          tmem_ld16(lane_addr + COL_Y + 3 * BN + c0 + ch, y11);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16 && live; ++j) {
-            const int f = n0 + ch + j;
+            const int f = n0 + c0 + ch + j;
             float* yf = y + ((size_t)n * F + f) * (size_t)d.oh * d.ow;
             const int oy = 2 * ty, ox = 2 * tx;
             const float v[2][2] = {{y00[j], y01[j]}, {y10[j], y11[j]}};
@@ -365,13 +378,13 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     const long long tot = clock64() - t_start;
     if (tid == 0) { TRACE(20, (int)(tot >> 10)); TRACE(21, (int)(w_cv_b >> 10)); TRACE(22, (int)(w_cv_a >> 10)); }
     if (tid == 128) TRACE(23, (int)(w_ep >> 10));
-    if (tid == 256) TRACE(24, (int)(w_tma >> 10));
-    if (tid == 288) { TRACE(25, (int)(w_mma_b >> 10)); TRACE(26, (int)(w_mma_acc >> 10)); TRACE(27, (int)(w_mma_a >> 10)); }
+    if (tid == 32 * WARP_TMA) TRACE(24, (int)(w_tma >> 10));
+    if (tid == 32 * WARP_MMA) { TRACE(25, (int)(w_mma_b >> 10)); TRACE(26, (int)(w_mma_acc >> 10)); TRACE(27, (int)(w_mma_a >> 10)); }
   }
 #endif
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<512>(tmem);
+  if (warp == WARP_MMA) tmem_dealloc<512>(tmem);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {

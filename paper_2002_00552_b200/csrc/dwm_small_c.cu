@@ -33,54 +33,15 @@
 
 #include "dwm_common.cuh"
 #include "dwm_kernels.h"
+#include "dwm_wino.cuh"
 
 namespace dwm {
 namespace {
 
+using namespace wino;
+
 constexpr int THREADS = 256;  // 32 tile lanes x 8 filter groups
 constexpr int MAXQ = 16;      // frequencies per part, (3+1)^2
-
-// At coefficient of F(2, r): row i (output), column a (frequency).
-__host__ __device__ constexpr int at_coef(int r, int i, int a) {
-  return r == 1 ? (i == a ? 1 : 0)
-       : r == 2 ? (i == 0 ? (a <= 1 ? 1 : 0) : (a == 1 ? 1 : (a == 2 ? -1 : 0)))
-                : (i == 0 ? (a <= 2 ? 1 : 0) : (a == 0 ? 0 : (a == 1 ? 1 : -1)));
-}
-// Bt coefficient of F(2, r): row a (frequency), column i (window sample).
-__host__ __device__ constexpr int bt_coef(int r, int a, int i) {
-  // F(2,1): I2;  F(2,2): [[1,-1,0],[0,1,0],[0,1,-1]];
-  // F(2,3): [[1,0,-1,0],[0,1,1,0],[0,-1,1,0],[0,1,0,-1]]
-  return r == 1 ? (a == i ? 1 : 0)
-       : r == 2 ? (a == 0 ? (i == 0 ? 1 : i == 1 ? -1 : 0)
-                  : a == 1 ? (i == 1 ? 1 : 0)
-                           : (i == 1 ? 1 : i == 2 ? -1 : 0))
-                : (a == 0 ? (i == 0 ? 1 : i == 2 ? -1 : 0)
-                  : a == 1 ? (i == 1 || i == 2 ? 1 : 0)
-                  : a == 2 ? (i == 1 ? -1 : i == 2 ? 1 : 0)
-                           : (i == 1 ? 1 : i == 3 ? -1 : 0));
-}
-// first index with a nonzero coefficient (the sequential sum starts there)
-__host__ __device__ constexpr int at_first(int r, int i) {
-  int k = 0;
-  while (at_coef(r, i, k) == 0) ++k;
-  return k;
-}
-__host__ __device__ constexpr int bt_first(int r, int a) {
-  int k = 0;
-  while (bt_coef(r, a, k) == 0) ++k;
-  return k;
-}
-
-// ---- scalar chain (producer): acc = sum_k K_k * m_k, K in {0, +-1} ---------
-// Zero terms are skipped and the first nonzero term is a move (BLAS starts from
-// +0, so only the sign of an exact zero can differ).  A leading -1 (Bt row 2
-// of F(2,3)) is carried as a negated accumulator and fixed by `finish`.
-template <int K, bool FIRST, bool NEG> __device__ __forceinline__ void chain(float& acc, float m) {
-  if constexpr (K == 0) return;
-  else if constexpr (FIRST) acc = m;  // value is K*m; sign kept in NEG
-  else if constexpr ((K == 1) != NEG) acc = __fadd_rn(acc, m);
-  else acc = __fsub_rn(acc, m);
-}
 
 // ---- packed f32x2 (two adjacent filters) ----------------------------------
 typedef unsigned long long f2;
@@ -120,14 +81,6 @@ template <int K, bool FIRST> __device__ __forceinline__ void chain2(f2& acc, f2 
   else if constexpr (FIRST) { static_assert(K == 1, "At rows start with +1"); acc = m; }
   else if constexpr (K == 1) acc = add2(acc, m);
   else acc = sub2(acc, m);
-}
-
-template <typename F, int... Is>
-__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {
-  (f(std::integral_constant<int, Is>{}), ...);
-}
-template <int N, typename F> __device__ __forceinline__ void static_for(F&& f) {
-  static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
 template <int CC_, int TM_, int TN_>
@@ -217,19 +170,6 @@ __device__ __forceinline__ void consume_part(const float* __restrict__ sV, const
         }
 }
 
-#define DWM_PART_SWITCH(pr, pc, CALL)            \
-  switch ((pr) * 4 + (pc)) {                     \
-    case 5: CALL(1, 1); break;                   \
-    case 6: CALL(1, 2); break;                   \
-    case 7: CALL(1, 3); break;                   \
-    case 9: CALL(2, 1); break;                   \
-    case 10: CALL(2, 2); break;                  \
-    case 11: CALL(2, 3); break;                  \
-    case 13: CALL(3, 1); break;                  \
-    case 14: CALL(3, 2); break;                  \
-    default: CALL(3, 3); break;                  \
-  }
-
 // Producer geometry of one (tile, channel) for a tile block, computed once.
 struct ProdTile {
   const float* xc;  // x[n][c]
@@ -276,38 +216,10 @@ __device__ __forceinline__ void load_window(const dwm_desc_t& d, const ProdTile&
       win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? __ldg(p.xc + rows[i] + cols[j]) : 0.f;
 }
 
-// Producer half 2: Bt.d.B (row stage then column stage, compile-time
-// coefficients) -> sV[q][c][t].
+// Producer half 2: Bt.d.B with compile-time coefficients -> sV[q][c][t].
 template <class K, int PR, int PC>
 __device__ __forceinline__ void transform_store(const float (&win)[4][4], float* __restrict__ sV, int t, int c) {
-  constexpr int LR = PR + 1, LC = PC + 1;
-  float tt[LR][LC];
-  static_for<LR>([&](auto aI) {
-    constexpr int a = decltype(aI)::value;
-    constexpr bool neg = bt_coef(PR, a, bt_first(PR, a)) < 0;
-    static_for<LR>([&](auto iI) {
-      constexpr int i = decltype(iI)::value;
-#pragma unroll
-      for (int j = 0; j < LC; ++j) chain<bt_coef(PR, a, i), (i == bt_first(PR, a)), neg>(tt[a][j], win[i][j]);
-    });
-    if constexpr (neg) {
-#pragma unroll
-      for (int j = 0; j < LC; ++j) tt[a][j] = -tt[a][j];
-    }
-  });
-  static_for<LR>([&](auto aI) {
-    constexpr int a = decltype(aI)::value;
-    static_for<LC>([&](auto bI) {
-      constexpr int b = decltype(bI)::value;
-      constexpr bool neg = bt_coef(PC, b, bt_first(PC, b)) < 0;
-      float v;
-      static_for<LC>([&](auto jI) {
-        constexpr int j = decltype(jI)::value;
-        chain<bt_coef(PC, b, j), (j == bt_first(PC, b)), neg>(v, tt[a][j]);
-      });
-      sV[((a * LC + b) * K::CC + c) * K::BM + t] = neg ? -v : v;
-    });
-  });
+  input_transform_part<PR, PC>(win, [&](int q, float v) { sV[(q * K::CC + c) * K::BM + t] = v; });
 }
 
 template <class K>

@@ -10,6 +10,7 @@
 // reference's binary32/binary64 values (the coefficients are 0, +-1, +-1/2).
 #include "dwm_common.cuh"
 #include "dwm_kernels.h"
+#include "dwm_wino.cuh"
 
 namespace dwm {
 
@@ -248,28 +249,11 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? sc[rows[i] + cols[j]] : T(0);
-        T t[4][4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            T acc = mul_rn((T)c_bt[pr][a][0], win[0][j]);
-#pragma unroll
-            for (int i = 1; i < 4; ++i)
-              if (i < lr) acc = fma_rn((T)c_bt[pr][a][i], win[i][j], acc);
-            t[a][j] = acc;
-          }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (a < lr && b < lc) {
-              T acc = mul_rn(t[a][0], (T)c_bt[pc][b][0]);
-#pragma unroll
-              for (int j = 1; j < 4; ++j)
-                if (j < lc) acc = fma_rn(t[a][j], (T)c_bt[pc][b][j], acc);
-              vout[(int64_t)(fq + a * lc + b) * tc_stride] = acc;
-            }
+        T* vq = vout + (int64_t)fq * tc_stride;
+        auto store = [&](int q, T v) { vq[(int64_t)q * tc_stride] = v; };
+#define DWM_ITP(A, B) wino::input_transform_part<A, B>(win, store)
+        DWM_PART_SWITCH(pr, pc, DWM_ITP)
+#undef DWM_ITP
         fq += lr * lc;
       }
     }
