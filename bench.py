@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--algo", default="auto", choices=["auto", "exact", "tc", "small_c"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=None, help="override per-GPU batch (debug only)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs the workload's batch; strong: the batch is sharded over ranks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -58,11 +60,40 @@ def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
-                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
-                "source": "measured (MEASURED_PEAKS.json)"}
-    return dict(FALLBACK_PEAKS, bf16_tflops_sustained=1400.0,
-                source="fallback (B200_PROFILING.md)")
+        out = {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+               "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+               "source": "measured (MEASURED_PEAKS.json)"}
+    else:
+        out = dict(FALLBACK_PEAKS, bf16_tflops_sustained=1400.0, source="fallback (B200_PROFILING.md)")
+    # TF32 tensor and FP32 FFMA peaks measured on this pool's B200s by our own
+    # microbenchmarks (tools/tc_probe.cu, tools/fp32_peak.cu); MEASURED_PEAKS has bf16 only
+    u = ROOT / "profiles" / "measured_unit_peaks.json"
+    if u.exists():
+        d = json.loads(u.read_text())
+        out["tf32_tflops"], out["fp32_tflops"] = float(d["tf32_tflops"]), float(d["fp32_ffma_tflops"])
+        out["unit_source"] = "measured (profiles/measured_unit_peaks.json)"
+    else:
+        out["tf32_tflops"], out["fp32_tflops"] = out["bf16_tflops"] / 2, 72.0
+        out["unit_source"] = "bf16/2 and nominal FP32"
+    return out
+
+
+def small_c_fp32_ops(desc) -> float:
+    """FP32 lane operations of the exact-order fused small-C kernel per step:
+    per (tile, filter) and part, C*a_r*a_c FMA/MUL (counted as 2 flops), the
+    At row/column stage adds and the part-sum adds (SURVEY §8d accounting)."""
+    at_nnz = {1: [1, 1], 2: [2, 2], 3: [3, 3]}  # nonzeros per At row
+    ops = 0.0
+    first = True
+    for rp in desc.axis("row"):
+        for cp in desc.axis("col"):
+            pr, pc = rp[2], cp[2]
+            ops += 2.0 * desc.c * (pr + 1) * (pc + 1)
+            ops += (pc + 1) * sum(n - 1 for n in at_nnz[pr])
+            ops += 2 * sum(n - 1 for n in at_nnz[pc])
+            ops += 0 if first else 4
+            first = False
+    return ops * desc.tiles * desc.f
 
 
 # ---------------------------------------------------------------------------
@@ -232,7 +263,13 @@ def main():
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     lib = _native.load()
-    batch = args.batch or wl.batch
+    from paper_2002_00552_b200.sharding import max_over_ranks, shard_range
+    global_batch = args.batch or wl.batch
+    if args.scaling == "strong":
+        lo, hi = shard_range(global_batch, rank, world)
+        batch = hi - lo
+    else:
+        batch = global_batch
     spec = wl.spec()
     desc = _native.make_desc(batch, wl.c_in, wl.hw, wl.hw, wl.c_out, spec.kernel, spec.stride, spec.pad)
     algo = _native.ALGOS[args.algo]
@@ -292,12 +329,8 @@ def main():
     if dist is not None:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    if dist is not None:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    images = batch * world * args.steps
+    total_ms = max_over_ranks(sum(step_ms), dist, dev)
+    images = (global_batch if args.scaling == "strong" else batch * world) * args.steps
     value = images / (total_ms / 1e3)
     launches_per_step = 2 if algo_name == "small_c" else 3
 
@@ -320,11 +353,12 @@ def main():
     line = {
         "metric": BASELINE_METRIC, "value": value, "unit": "images/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) (torch.randn on device)",
         "config": {"workload": wl.name, "kernel": wl.kernel, "stride": wl.stride, "pad": wl.pad,
                    "hw": wl.hw, "c_in": wl.c_in, "c_out": wl.c_out, "batch_per_gpu": batch,
-                   "global_batch": batch * world, "out_hw": [desc.oh, desc.ow],
+                   "global_batch": global_batch if args.scaling == "strong" else batch * world,
+                   "out_hw": [desc.oh, desc.ow],
                    "parts": desc.n_row_parts * desc.n_col_parts, "frequencies": desc.num_freqs,
                    "engine": algo_name,
                    "l2": ("inputs+intermediates > L2 (%.2f GB/step)" % (working_set / 1e9)
@@ -419,18 +453,24 @@ def make_roofline(stage_ms, desc, wl, batch, algo_name, peaks, x_bytes, w_bytes,
     top = max(kernels, key=lambda k: k["ms"])
     traffic = lookup_traffic(wl.name, top["name"])
     if top["name"] == "gemm_output" and algo_name == "tc":
-        peak_tf32 = peaks["bf16_tflops"] / 2
+        peak_tf32 = peaks["tf32_tflops"]
         achieved = 3 * gemm_flops / (top["ms"] * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": top["name"], "achieved": achieved,
                 "peak": peak_tf32, "unit": "TFLOP/s", "frac": achieved / peak_tf32,
                 "traffic": traffic,
-                "note": "3xTF32 tensor FLOPs (3 x 2*C*F*tiles*freqs) vs TF32 dense peak = measured bf16/2, "
-                        + peaks["source"]}
+                "note": "3xTF32 tensor FLOPs (3 x 2*C*F*tiles*freqs) vs dense TF32 tcgen05 peak, "
+                        + peaks["unit_source"]}
     else:
         achieved = top["alg_bytes"] / (top["ms"] * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": top["name"], "achieved": achieved, "peak": hbm,
                 "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                 "note": "algorithmic bytes per launch / CUDA-event time vs " + peaks["source"]}
+        if top["name"] == "conv2d_small_c":
+            fp = small_c_fp32_ops(desc) / (top["ms"] * 1e-3) / 1e12
+            roof["fp32_pipe"] = {"achieved": fp, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
+                                 "frac": fp / peaks["fp32_tflops"],
+                                 "note": "C_in<=4: the binding unit is the FP32 pipe (exact reference "
+                                         "rounding order on CUDA cores), " + peaks["unit_source"]}
     return roof, kernels
 
 
@@ -462,11 +502,8 @@ def run_e2e(args, wl, spec, batch, dev, dist, world, dwm_conv2d):
     for _ in range(steps):
         dwm_conv2d(xh, wh, spec, out=yh)
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    if dist is not None:
-        t = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
+    from paper_2002_00552_b200.sharding import max_over_ranks
+    dt = max_over_ranks(time.perf_counter() - t0, dist, dev)
     return {"value": batch * world * steps / dt, "unit": "images/s",
             "h2d_bytes_per_step": (xh.numel() + wh.numel()) * 4,
             "d2h_bytes_per_step": yh.numel() * 4 + 4, "steps": steps,
