@@ -162,10 +162,19 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           const uint32_t s = it % B_STAGES, round = it / B_STAGES;
           TWAIT(w_tma, &S.b_empty[s], (round & 1) ^ 1);
           if (elect_one()) {
+#if defined(DWM_EXP_NO_V_LOAD)
+            mbar_arrive_expect_tx(&S.b_full[s], 2 * U_TILE_BYTES);
+            tma_load_2d(S.u_hi[s], &map_uhi, &S.b_full[s], kc * BK, q * F + n0);
+            tma_load_2d(S.u_lo[s], &map_ulo, &S.b_full[s], kc * BK, q * F + n0);
+#elif defined(DWM_EXP_NO_U_LOAD)
+            mbar_arrive_expect_tx(&S.b_full[s], V_TILE_BYTES);
+            tma_load_3d(S.v[s], &map_v, &S.b_full[s], kc * BK, m0, q);
+#else
             mbar_arrive_expect_tx(&S.b_full[s], V_TILE_BYTES + 2 * U_TILE_BYTES);
             tma_load_3d(S.v[s], &map_v, &S.b_full[s], kc * BK, m0, q);
             tma_load_2d(S.u_hi[s], &map_uhi, &S.b_full[s], kc * BK, q * F + n0);
             tma_load_2d(S.u_lo[s], &map_ulo, &S.b_full[s], kc * BK, q * F + n0);
+#endif
           }
           __syncwarp();
         }
@@ -231,9 +240,12 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float h = tf32_rn(xs[e]);
+              // hi = tf32 round-to-nearest (ties away) in 2 integer ops; lo = x - hi
+              // exactly, handed to the tensor core raw (it truncates lo to tf32:
+              // emulated MSE identical to an RN lo, tools/../DESIGN.md §3.1)
+              const float h = __uint_as_float((__float_as_uint(xs[e]) + 0x1000u) & 0xFFFFE000u);
               hi[c4 * 4 + e] = h;
-              lo[c4 * 4 + e] = tf32_rn(xs[e] - h);
+              lo[c4 * 4 + e] = __fsub_rn(xs[e], h);
             }
           }
           __syncwarp();
@@ -244,11 +256,15 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             TWAIT(w_cv_a, &S.a_empty[sa], ((ita2 / A_STAGES) & 1) ^ 1);
             tc_fence_after();
             const uint32_t base = lane_addr + COL_A + sa * (2 * AK);
+#ifndef DWM_EXP_NO_CONV_ST
 #pragma unroll
             for (int c = 0; c < AK; c += 16) {
               tmem_st16(base + c, *reinterpret_cast<float(*)[16]>(hi + h * AK + c));
               tmem_st16(base + AK + c, *reinterpret_cast<float(*)[16]>(lo + h * AK + c));
             }
+#else
+            if (hi[0] == 12345.f) tmem_st16(base, *reinterpret_cast<float(*)[16]>(hi));
+#endif
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -306,6 +322,9 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         const int8_t cf[4] = {S.coef[q][0], S.coef[q][1], S.coef[q][2], S.coef[q][3]};
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
+#ifdef DWM_EXP_NO_EPI_Y
+          if (mq[0] != 12345.f) continue;
+#endif
           if (cf[p] == 0) continue;
           float yv[EC];
           const uint32_t ya = lane_addr + COL_Y + p * BN + c0;

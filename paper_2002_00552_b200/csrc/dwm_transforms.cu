@@ -198,19 +198,25 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   extern __shared__ __align__(16) unsigned char it_smem_raw[];
   T* sx = reinterpret_cast<T*>(it_smem_raw);  // [IT_CB][rows_staged][W] with odd channel pitch
   const int pitch = rows_staged * d.w + 1;
-  const int ty = blockIdx.x % d.th;
-  const int n = blockIdx.x / d.th;
-  const int c0 = blockIdx.y * IT_CB;
+  // channel block fastest: the C/32 CTAs of one tile row run together
+  const int ty = blockIdx.y % d.th;
+  const int n = blockIdx.y / d.th;
+  const int c0 = blockIdx.x * IT_CB;
   const int cb = min(IT_CB, d.c - c0);
   const int row0 = 2 * ty * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
 
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
   for (int cc = threadIdx.x / 32; cc < cb; cc += blockDim.x / 32) {
     const T* xc = x + ((int64_t)n * d.c + c0 + cc) * d.h * d.w;
-    for (int e = threadIdx.x % 32; e < rows_staged * d.w; e += 32) {
-      const int r = e / d.w, col = e % d.w;
+    T* dst = sx + cc * pitch;
+    for (int r = 0; r < rows_staged; ++r) {
       const int row = row0 + r;
-      sx[cc * pitch + e] = (row >= 0 && row < d.h) ? __ldg(xc + (int64_t)row * d.w + col) : T(0);
+      if (row >= 0 && row < d.h) {
+        const T* src = xc + (int64_t)row * d.w;
+        for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = __ldg(src + col);
+      } else {
+        for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = T(0);
+      }
     }
   }
   __syncthreads();
@@ -290,7 +296,7 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   if (smem > 96 * 1024 || d.c < 8) return DWM_OK;
   DWM_CUDA_TRY(cudaFuncSetAttribute(input_transform_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-  const dim3 grid((unsigned)((int64_t)d.n * d.th), (unsigned)((d.c + IT_CB - 1) / IT_CB));
+  const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)((int64_t)d.n * d.th));
   input_transform_smem_kernel<T><<<grid, 256, smem, s>>>(d, (const T*)x, (T*)V, rows);
   DWM_CUDA_TRY(cudaGetLastError());
   *used = true;
