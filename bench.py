@@ -451,7 +451,7 @@ def make_roofline(stage_ms, desc, wl, batch, algo_name, peaks, x_bytes, w_bytes,
     for k in kernels:
         k["share"] = k["ms"] / total
     top = max(kernels, key=lambda k: k["ms"])
-    traffic = lookup_traffic(wl.name, top["name"])
+    traffic = lookup_traffic(wl.name, top["name"], batch)
     if top["name"] == "gemm_output" and algo_name == "tc":
         peak_tf32 = peaks["tf32_tflops"]
         achieved = 3 * gemm_flops / (top["ms"] * 1e-3) / 1e12
@@ -474,14 +474,20 @@ def make_roofline(stage_ms, desc, wl, batch, algo_name, peaks, x_bytes, w_bytes,
     return roof, kernels
 
 
-def lookup_traffic(workload, kernel):
+def lookup_traffic(workload, kernel, batch):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    this kernel from the committed ncu --set full capture, scaled per image to
+    this launch's batch; None when no capture exists for the workload."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(workload, {}).get(kernel)
+        e = json.loads(p.read_text()).get(workload, {}).get(kernel)
     except (ValueError, OSError):
         return None
+    if not e:
+        return None
+    return e["bytes_per_image"] * batch
 
 
 def run_e2e(args, wl, spec, batch, dev, dist, world, dwm_conv2d):
