@@ -303,9 +303,8 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           TWAIT(w_ep, &S.acc_full[ab], (itq / 2) & 1);
           tc_fence_after();
           float part[EC];
-#pragma unroll
-          for (int ch = 0; ch < EC; ch += 16)
-            tmem_ld16(lane_addr + COL_ACC + ab * BN + c0 + ch, *reinterpret_cast<float(*)[16]>(part + ch));
+          static_assert(EC == 32, "one x32 TMEM load per epilogue warp and chunk");
+          tmem_ld32(lane_addr + COL_ACC + ab * BN + c0, part);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
@@ -328,8 +327,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           if (cf[p] == 0) continue;
           float yv[EC];
           const uint32_t ya = lane_addr + COL_Y + p * BN + c0;
-#pragma unroll
-          for (int ch = 0; ch < EC; ch += 16) tmem_ld16(ya + ch, *reinterpret_cast<float(*)[16]>(yv + ch));
+          tmem_ld32(ya, yv);
           tmem_ld_wait();
           if (cf[p] > 0) {
 #pragma unroll
