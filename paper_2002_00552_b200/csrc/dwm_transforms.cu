@@ -192,6 +192,22 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
 // ---------------------------------------------------------------------------
 constexpr int IT_CB = 32;  // channels per CTA (one per lane)
 
+// Window gather (compile-time extent, predicated zeros) + Bt.d.B + stores
+// to consecutive frequency planes through a running pointer.
+template <int PR, int PC, typename T>
+__device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const int (&rows)[4], const int (&cols)[4],
+                                               T* vq, int64_t stride) {
+  T win[4][4];
+#pragma unroll
+  for (int i = 0; i <= PR; ++i)
+#pragma unroll
+    for (int j = 0; j <= PC; ++j) win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? sc[rows[i] + cols[j]] : T(0);
+  wino::input_transform_part<PR, PC>(win, [&](int, T v) {
+    *vq = v;
+    vq += stride;
+  });
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged) {
@@ -250,14 +266,8 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
           const int col = Cc.origin + d.s_w * k - d.pad_left;
           cols[j] = (j < lc && k < d.ow - 1 + pc && col >= 0 && col < d.w) ? col : -1;
         }
-        T win[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? sc[rows[i] + cols[j]] : T(0);
         T* vq = vout + (int64_t)fq * tc_stride;
-        auto store = [&](int q, T v) { vq[(int64_t)q * tc_stride] = v; };
-#define DWM_ITP(A, B) wino::input_transform_part<A, B>(win, store)
+#define DWM_ITP(A, B) it_gather_part<A, B>(sc, rows, cols, vq, tc_stride)
         DWM_PART_SWITCH(pr, pc, DWM_ITP)
 #undef DWM_ITP
         fq += lr * lc;
