@@ -12,6 +12,8 @@
 #include "dwm_kernels.h"
 #include "dwm_wino.cuh"
 
+#include <cstring>
+
 namespace dwm {
 
 // ---------------------------------------------------------------------------
@@ -222,16 +224,50 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   const int row0 = 2 * ty * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
 
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
-  for (int cc = threadIdx.x / 32; cc < cb; cc += blockDim.x / 32) {
-    const T* xc = x + ((int64_t)n * d.c + c0 + cc) * d.h * d.w;
-    T* dst = sx + cc * pitch;
-    for (int r = 0; r < rows_staged; ++r) {
-      const int row = row0 + r;
-      if (row >= 0 && row < d.h) {
-        const T* src = xc + (int64_t)row * d.w;
-        for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = __ldg(src + col);
-      } else {
-        for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = T(0);
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int SLOTS = 4;  // (row, vector) slots per lane: up to 128 float4 per channel row block
+  if (d.w % VEC == 0 && rows_staged * (d.w / VEC) <= 32 * SLOTS) {
+    // 16-byte loads; each lane owns fixed (row, vector) slots of the staged block
+    const int wv = d.w / VEC, nslots = rows_staged * wv;
+    const int lane = threadIdx.x % 32;
+    int srow[SLOTS], scol[SLOTS];
+#pragma unroll
+    for (int k = 0; k < SLOTS; ++k) {
+      const int p = lane + 32 * k;
+      srow[k] = p < nslots ? p / wv : -1;
+      scol[k] = p < nslots ? (p % wv) * VEC : 0;
+    }
+    for (int cc = threadIdx.x / 32; cc < cb; cc += blockDim.x / 32) {
+      const T* xc = x + ((int64_t)n * d.c + c0 + cc) * d.h * d.w;
+      T* dst = sx + cc * pitch;
+#pragma unroll
+      for (int k = 0; k < SLOTS; ++k) {
+        if (srow[k] < 0) continue;
+        const int row = row0 + srow[k];
+        T v[VEC];
+        if (row >= 0 && row < d.h) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(xc + (int64_t)row * d.w + scol[k]));
+          memcpy(v, &q, 16);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) v[e] = T(0);
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) dst[srow[k] * d.w + scol[k] + e] = v[e];
+      }
+    }
+  } else {
+    for (int cc = threadIdx.x / 32; cc < cb; cc += blockDim.x / 32) {
+      const T* xc = x + ((int64_t)n * d.c + c0 + cc) * d.h * d.w;
+      T* dst = sx + cc * pitch;
+      for (int r = 0; r < rows_staged; ++r) {
+        const int row = row0 + r;
+        if (row >= 0 && row < d.h) {
+          const T* src = xc + (int64_t)row * d.w;
+          for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = __ldg(src + col);
+        } else {
+          for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = T(0);
+        }
       }
     }
   }
@@ -307,7 +343,13 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   DWM_CUDA_TRY(cudaFuncSetAttribute(input_transform_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
   const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)((int64_t)d.n * d.th));
-  input_transform_smem_kernel<T><<<grid, 256, smem, s>>>(d, (const T*)x, (T*)V, rows);
+  // warps: a divisor of the tile-row length in [4, 8] so every warp gets the same number of tiles
+  int warps = 8;
+  if (d.tw <= 8) warps = d.tw;
+  else
+    for (int cand = 8; cand >= 4; --cand)
+      if (d.tw % cand == 0) { warps = cand; break; }
+  input_transform_smem_kernel<T><<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows);
   DWM_CUDA_TRY(cudaGetLastError());
   *used = true;
   return DWM_OK;
