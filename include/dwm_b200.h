@@ -121,6 +121,28 @@ int dwm_gemm_output(const dwm_desc_t* desc, int dtype, int algo, const void* V,
 int dwm_conv2d_small_c(const dwm_desc_t* desc, const void* x, const void* U,
                        void* y, int32_t* nonfinite_flag, void* stream);
 
+/* Cached-filter forward (the operator wrapper keeps U
+ * per weight version; the reference recomputes G g G^T every call,
+ * engines.py:246-248).  dwm_filter_bytes: bytes of U in the layout the
+ * engine `algo` selects for this geometry (TC: hi|lo TF32 planes).  U depends
+ * only on (F, C, kernel, stride, algo), never on the batch or image size --
+ * but the selected engine can, so prepare with the same desc as the forward.
+ * dwm_conv2d_forward_prepared: the forward with U given; workspace holds V
+ * only (dwm_workspace_bytes is an upper bound). */
+size_t dwm_filter_bytes(const dwm_desc_t* desc, int dtype, int algo);
+int dwm_prepare_filter(const dwm_desc_t* desc, int dtype, int algo, const void* w,
+                       void* U, void* stream);
+int dwm_conv2d_forward_prepared(const dwm_desc_t* desc, int dtype, int algo, const void* x,
+                                const void* U, void* y, void* workspace, size_t workspace_bytes,
+                                int32_t* nonfinite_flag, void* stream);
+
+/* Weight gradient of the forward (reference
+ * dwm_backward, engines.py:342-399): gw[F,C,r_h,r_w] from x[N,C,H,W] and
+ * dy[N,F,OH,OW]; deterministic fixed-order reduction.  (The data gradient is
+ * computed by the forward engine on the adjoint problem, see engines.py.) */
+int dwm_weight_grad(const dwm_desc_t* desc, int dtype, const void* x, const void* dy,
+                    void* gw, void* stream);
+
 /* Whole forward: y[N,F,OH,OW] = dwm_conv2d(x[N,C,H,W], w[F,C,r_h,r_w]).
  * nonfinite_flag (device int32, may be NULL) is set to 1 when any output
  * is NaN/Inf; the caller raises FloatingPointError after syncing. */

@@ -173,6 +173,11 @@ int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, con
   return launch_gemm_exact(*d, dtype, V, U, y, flag, (cudaStream_t)stream);
 }
 
+int dwm_weight_grad(const dwm_desc_t* d, int dtype, const void* x, const void* dy, void* gw, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  return launch_weight_grad(*d, dtype, x, dy, gw, (cudaStream_t)stream);
+}
+
 int dwm_conv2d_small_c(const dwm_desc_t* d, const void* x, const void* U, void* y, int32_t* flag,
                        void* stream) {
   if (int st = check_common(d, DWM_F32)) return st;
@@ -203,6 +208,38 @@ int dwm_conv2d_forward(const dwm_desc_t* d, int dtype, int algo, const void* x, 
   if ((st = launch_input_transform(*d, dtype, x, V, s))) return st;
   if (sel == DWM_ALGO_TC) return launch_gemm_tc(*d, V, U, y, flag, s);
   return launch_gemm_exact(*d, dtype, V, U, y, flag, s);
+}
+
+size_t dwm_filter_bytes(const dwm_desc_t* d, int dtype, int algo) {
+  if (!d) return 0;
+  const size_t es = dtype == DWM_F64 ? 8 : 4;
+  size_t u = (size_t)d->num_freqs * (size_t)d->f * (size_t)d->c * es;
+  if (dwm_select_algo(d, dtype, algo) == DWM_ALGO_TC) u *= 2;
+  return u;
+}
+
+int dwm_prepare_filter(const dwm_desc_t* d, int dtype, int algo, const void* w, void* U, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  const int sel = dwm_select_algo(d, dtype, algo);
+  if (sel < 0) return bad_algo(d, algo);
+  if (sel == DWM_ALGO_TC) return launch_filter_transform_tf32split(*d, w, U, (cudaStream_t)stream);
+  return launch_filter_transform(*d, dtype, w, U, (cudaStream_t)stream);
+}
+
+int dwm_conv2d_forward_prepared(const dwm_desc_t* d, int dtype, int algo, const void* x, const void* U,
+                                void* y, void* ws, size_t ws_bytes, int32_t* flag, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  const int sel = dwm_select_algo(d, dtype, algo);
+  if (sel < 0) return bad_algo(d, algo);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (sel == DWM_ALGO_SMALL_C) return launch_small_c(*d, x, U, y, flag, s);
+  const size_t need = v_bytes_of(d, dtype == DWM_F64 ? 8 : 4);
+  if (!ws || ws_bytes < need)
+    return fail(DWM_EINVAL_SHAPE, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
+  int st;
+  if ((st = launch_input_transform(*d, dtype, x, ws, s))) return st;
+  if (sel == DWM_ALGO_TC) return launch_gemm_tc(*d, ws, U, y, flag, s);
+  return launch_gemm_exact(*d, dtype, ws, U, y, flag, s);
 }
 
 }  // extern "C"

@@ -391,8 +391,13 @@ int launch_cc(const dwm_desc_t& d, const float* x, const float* U, float* y, int
 bool small_c_supported(const dwm_desc_t& d) {
   if (d.c < 1 || d.c > 4) return false;
   if (d.tiles + 256 >= (int64_t)1 << 31) return false;  // 32-bit tile indexing
-  const size_t narrow = ((size_t)16 * 2 * THREADS + 2 * (size_t)MAXQ * d.c * 128 + (size_t)d.num_freqs * d.c * 32) *
-                        sizeof(float);
+  size_t narrow = 0;  // the fallback variant's shared memory (resident U grows with the freqs)
+  switch (d.c) {
+    case 1: narrow = Cfg<1, 4, 4>::smem_bytes(d.num_freqs); break;
+    case 2: narrow = Cfg<2, 4, 4>::smem_bytes(d.num_freqs); break;
+    case 3: narrow = Cfg<3, 4, 4>::smem_bytes(d.num_freqs); break;
+    default: narrow = Cfg<4, 4, 4>::smem_bytes(d.num_freqs); break;
+  }
   return narrow <= SMEM_CAP;
 }
 

@@ -370,3 +370,67 @@ int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* 
 }
 
 }  // namespace dwm
+
+namespace dwm {
+
+// ---------------------------------------------------------------------------
+// Weight gradient: dW[f,c,ky,kx] = sum_{n,oy,ox}
+// dY[n,f,oy,ox] * x_pad[n,c,s_h*oy+ky,s_w*ox+kx].  One warp per (f, c, ky):
+// lanes stride over (n, oy, ox) in a fixed order, kx taps in registers, then a
+// fixed-order warp-shuffle reduction -- deterministic run to run.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) weight_grad_kernel(const dwm_desc_t d, const T* __restrict__ x,
+                                                          const T* __restrict__ dy, T* __restrict__ gw) {
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int64_t nw = (int64_t)d.f * d.c * d.r_h;
+  if (wid >= nw) return;
+  const int ky = (int)(wid % d.r_h);
+  const int c = (int)((wid / d.r_h) % d.c);
+  const int f = (int)(wid / ((int64_t)d.r_h * d.c));
+  constexpr int MAXR = 16;
+  T acc[MAXR];
+#pragma unroll
+  for (int k = 0; k < MAXR; ++k) acc[k] = T(0);
+  const int64_t per_img = (int64_t)d.oh * d.ow;
+  const int64_t total = (int64_t)d.n * per_img;
+  for (int64_t e = lane; e < total; e += 32) {
+    const int n = (int)(e / per_img);
+    const int rem = (int)(e % per_img);
+    const int oy = rem / d.ow, ox = rem % d.ow;
+    const T g = dy[(((int64_t)n * d.f + f) * d.oh + oy) * d.ow + ox];
+    const int row = d.s_h * oy + ky - d.pad_top;
+    if (row < 0 || row >= d.h) continue;
+    const T* xr = x + (((int64_t)n * d.c + c) * d.h + row) * d.w;
+    const int col0 = d.s_w * ox - d.pad_left;
+#pragma unroll
+    for (int kx = 0; kx < MAXR; ++kx) {
+      if (kx >= d.r_w) break;
+      const int col = col0 + kx;
+      if (col >= 0 && col < d.w) acc[kx] = fma_rn(g, xr[col], acc[kx]);
+    }
+  }
+#pragma unroll
+  for (int kx = 0; kx < MAXR; ++kx) {
+    if (kx >= d.r_w) break;
+    T v = acc[kx];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = add_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) gw[((((int64_t)f * d.c + c) * d.r_h) + ky) * d.r_w + kx] = v;
+  }
+}
+
+int launch_weight_grad(const dwm_desc_t& d, int dtype, const void* x, const void* dy, void* gw, cudaStream_t s) {
+  if (d.r_w > 16) return fail(DWM_EUNSUPPORTED, "weight gradient kernel supports r_w <= 16, got %d", d.r_w);
+  const int64_t warps = (int64_t)d.f * d.c * d.r_h;
+  const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+  if (dtype == DWM_F64)
+    weight_grad_kernel<double><<<grid, 256, 0, s>>>(d, (const double*)x, (const double*)dy, (double*)gw);
+  else
+    weight_grad_kernel<float><<<grid, 256, 0, s>>>(d, (const float*)x, (const float*)dy, (float*)gw);
+  DWM_CUDA_TRY(cudaGetLastError());
+  return DWM_OK;
+}
+
+}  // namespace dwm

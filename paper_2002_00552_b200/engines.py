@@ -246,6 +246,92 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
     s_out.synchronize()
 
 
+def _to_device(x, dev, tdt):
+    torch = _torch()
+    t = torch.from_numpy(np.ascontiguousarray(x)) if not _is_torch(x) else x
+    return t.to(dev, dtype=tdt).contiguous()
+
+
+def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=None, *,
+                 algo: str = "auto", stream=None):
+    """Gradients of ``dwm_conv2d`` w.r.t. data and weights on B200 (SURVEY §8f
+    rank 1; reference ``engines.py:342-399``, same signature, checks and
+    messages).  Returns ``(grad_data, grad_weights)``.
+
+    B200 design (not the reference's per-part Winograd adjoint):
+
+    * data gradient -- the adjoint of a stride-s correlation is a stride-1
+      correlation of the s-dilated ``grad_out`` with the 180-degree-rotated,
+      channel-transposed kernel.  That is itself a DWM forward, so it runs on
+      the forward engine (tcgen05 3xTF32 when the channel counts allow);
+      padding of the adjoint problem is ``r-1-pad`` (negative -> crop).
+    * weight gradient -- ``dwm_weight_grad`` (C ABI): a deterministic
+      fixed-order reduction over (image, output row, output column) per
+      (filter, channel, tap row) warp.
+
+    Both are exact in exact arithmetic, so results agree with the reference's
+    to rounding (binary64: <= 1e-10 absolute, the reference's own criterion).
+    """
+    _check_pair(data, weights)
+    _require_tensor4(grad_out, "grad_out")
+    spec = plan.spec
+    if tuple(weights.shape[2:]) != spec.kernel:
+        raise ValueError(f"weights taps {tuple(weights.shape[2:])} do not match kernel {spec.kernel}")
+    n, c, h, w = (int(s) for s in data.shape)
+    f = int(weights.shape[0])
+    oh, ow = spec.out_dims(h, w)
+    if tuple(grad_out.shape) != (n, f, oh, ow):
+        raise ValueError(f"grad_out shape {tuple(grad_out.shape)} != {(n, f, oh, ow)}")
+    dt = _np_dtype(grad_out) if precision is None else precision_dtype(precision)
+
+    torch = _torch()
+    lib = _native.load()
+    if not torch.cuda.is_available():
+        raise _native.NativeError("dwm_backward needs a CUDA device (B200); there is no CPU fallback")
+    tdt = torch.float64 if dt == np.dtype(np.float64) else torch.float32
+    code = _native.DWM_F64 if tdt == torch.float64 else _native.DWM_F32
+    cuda_in = _is_torch(grad_out) and grad_out.is_cuda
+    dev = grad_out.device if cuda_in else torch.device("cuda", torch.cuda.current_device())
+    r_h, r_w = spec.kernel
+    s_h, s_w = spec.stride
+    top, _, left, _ = spec.pad
+
+    with torch.cuda.device(dev):
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(s):
+            dy = _to_device(grad_out, dev, tdt)
+            x = _to_device(data, dev, tdt)
+            wt = _to_device(weights, dev, tdt)
+
+            gw = torch.empty((f, c, r_h, r_w), dtype=tdt, device=dev)
+            desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+            _native.check(lib.dwm_weight_grad(desc, code, x.data_ptr(), dy.data_ptr(), gw.data_ptr(),
+                                              s.cuda_stream), "dwm_weight_grad")
+
+            hd, wd = s_h * (oh - 1) + 1, s_w * (ow - 1) + 1
+            if (s_h, s_w) != (1, 1):
+                dil = torch.zeros((n, f, hd, wd), dtype=tdt, device=dev)
+                dil[:, :, ::s_h, ::s_w] = dy
+            else:
+                dil = dy
+            pt, pb = r_h - 1 - top, h + top - hd
+            pl, pr = r_w - 1 - left, w + left - wd
+            if min(pt, pb, pl, pr) < 0:
+                dil = dil[:, :, max(0, -pt):dil.shape[2] - max(0, -pb),
+                          max(0, -pl):dil.shape[3] - max(0, -pr)]
+                pt, pb, pl, pr = (max(0, p) for p in (pt, pb, pl, pr))
+            w_adj = wt.flip(2, 3).transpose(0, 1).contiguous()
+            adj = ConvSpec(kernel=spec.kernel, stride=(1, 1), pad=(pt, pb, pl, pr))
+            gd = dwm_conv2d(dil.contiguous(), w_adj, adj, algo=algo, check_finite=False, stream=s)
+            if not (bool(torch.isfinite(gd).all()) and bool(torch.isfinite(gw).all())):
+                raise FloatingPointError("dwm_backward produced non-finite values")
+    if not _is_torch(grad_out):
+        return gd.cpu().numpy(), gw.cpu().numpy()
+    if not cuda_in:
+        return gd.cpu(), gw.cpu()
+    return gd, gw
+
+
 def convolve(data, weights, spec: ConvSpec, algo: str = "dwm", precision=None,
              plan: DecompositionPlan = None) -> ConvOutput:
     """Instrumented run by name (reference engines.py:402-421); only "dwm"

@@ -15,6 +15,10 @@ and writes:
   baseline_samples.json  per BASELINE workload (one image, seed 1, the bench.py
                       _draw recipe): reference DWM32 / direct32 MSE vs direct64
                       and 512 sampled output values of DWM32 and direct64
+  backward_cases.npz  inputs + reference dwm_backward (binary64 and binary32)
+  backward_cases.json on the reference's backward test geometries plus
+                      asymmetric/rectangular/channel-heavy extras
+                      (``make_golden.py backward`` regenerates only these)
 The GPU box has no /root/reference; the tests there read these files.
 """
 
@@ -31,7 +35,7 @@ sys.dont_write_bytecode = True
 
 from dwmconv.convspec import ConvSpec  # noqa: E402
 from dwmconv.decompose import plan_decomposition, plan_to_json  # noqa: E402
-from dwmconv.engines import direct_conv2d, dwm_conv2d  # noqa: E402
+from dwmconv.engines import direct_conv2d, dwm_backward, dwm_conv2d  # noqa: E402
 from dwmconv.tensor import mse  # noqa: E402
 from dwmconv.transforms import get_transform, transform_to_json  # noqa: E402
 
@@ -141,7 +145,59 @@ def baseline_samples():
     (HERE / "baseline_samples.json").write_text(json.dumps(out))
 
 
+def backward_case_specs():
+    cases = []
+    # test_engines_backward.py:81-98 (+ the finite-difference and degenerate cases)
+    for k, s, p in [((3, 3), (1, 1), (1, 1, 1, 1)), ((5, 5), (1, 1), (2, 2, 2, 2)),
+                    ((5, 5), (2, 2), (1, 1, 1, 1)), ((7, 7), (2, 2), (3, 3, 3, 3))]:
+        cases.append(dict(name=f"bw_r{k[0]}_s{s[0]}", seed=sum(k) + sum(s), kernel=k, stride=s, pad=p,
+                          shape=(2, 2, 12, 12), f=2))
+    cases.append(dict(name="bw_fd", seed=23, kernel=(5, 5), stride=(2, 2), pad=(1, 1, 1, 1),
+                      shape=(1, 2, 9, 9), f=2))
+    cases.append(dict(name="bw_degenerate", seed=21, kernel=(3, 3), stride=(1, 1), pad=(0, 0, 0, 0),
+                      shape=(1, 2, 8, 8), f=2))
+    extra = [((11, 11), (4, 4), (2, 2, 2, 2), (1, 3, 31, 31), 4),
+             ((4, 6), (2, 1), (1, 2, 0, 3), (2, 3, 13, 11), 3),
+             ((7, 3), (1, 3), (3, 3, 1, 1), (1, 4, 12, 17), 5),
+             ((5, 5), (2, 2), (0, 0, 0, 0), (1, 2, 8, 8), 2),      # unused trailing row/col
+             ((3, 3), (1, 1), (4, 0, 0, 3), (1, 2, 7, 6), 2),      # pad > r-1 (adjoint crops)
+             ((1, 1), (3, 2), (0, 0, 0, 0), (1, 3, 9, 8), 2),
+             ((7, 7), (2, 2), (3, 3, 3, 3), (2, 3, 20, 20), 64),   # ResNet stem shape, small
+             ((3, 3), (1, 1), (1, 1, 1, 1), (1, 64, 10, 10), 64),  # tensor-core adjoint
+             ((5, 5), (1, 1), (2, 2, 2, 2), (1, 32, 9, 9), 128)]
+    for i, (k, s, p, shp, f) in enumerate(extra):
+        cases.append(dict(name=f"bw_extra{i}", seed=900 + i, kernel=k, stride=s, pad=p, shape=shp, f=f))
+    return cases
+
+
+def backward_cases():
+    arrays = {}
+    meta = []
+    for case in backward_case_specs():
+        rng = np.random.default_rng(case["seed"])
+        n, c, h, w = case["shape"]
+        spec = ConvSpec(kernel=case["kernel"], stride=case["stride"], pad=case["pad"])
+        d = rng.standard_normal((n, c, h, w))
+        g = rng.standard_normal((case["f"], c, *case["kernel"]))
+        oh, ow = spec.out_dims(h, w)
+        dy = rng.standard_normal((n, case["f"], oh, ow))
+        plan = plan_decomposition(spec)
+        key = case["name"]
+        arrays[f"{key}/data"] = d
+        arrays[f"{key}/weights"] = g
+        arrays[f"{key}/grad_out"] = dy
+        arrays[f"{key}/gd64"], arrays[f"{key}/gw64"] = dwm_backward(dy, plan, d, g, precision=np.float64)
+        arrays[f"{key}/gd32"], arrays[f"{key}/gw32"] = dwm_backward(dy, plan, d, g, precision=np.float32)
+        meta.append({k: (list(v) if isinstance(v, tuple) else v) for k, v in case.items()})
+    np.savez_compressed(HERE / "backward_cases.npz", **arrays)
+    (HERE / "backward_cases.json").write_text(json.dumps(meta, indent=1))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["backward"]:
+        backward_cases()
+        sys.exit(0)
+    backward_cases()
     plans()
     transforms()
     small_cases()

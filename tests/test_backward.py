@@ -1,0 +1,159 @@
+"""DWM backward: ``dwm_backward`` against the reference's
+own ``dwm_backward`` outputs (golden fixtures made by tests/golden/make_golden.py
+on the reference's backward test geometries, test_engines_backward.py:81-132)
+and against the binary64 analytic oracle.
+
+Tolerances (written here):
+  * binary64: max |gpu - oracle| <= 1e-10 (the reference's own criterion,
+    test_engines_backward.py:96-97) and max |gpu - reference dwm64| <= 1e-10.
+  * binary32: MSE vs the binary64 oracle <= 4 x the reference's binary32 MSE
+    (plus 1e-14 absolute for the all-but-exact tiny cases) -- the B200 data
+    gradient runs the forward engine on the adjoint problem and the weight
+    gradient is a different (fixed) summation order, so bits differ but the
+    error must stay at the reference's level.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle.dwm_oracle import direct_conv2d_grads_f64, mse
+from paper_2002_00552_b200 import ConvSpec, dwm_backward, plan_decomposition
+
+CASES = json.loads((GOLDEN / "backward_cases.json").read_text())
+ARR = np.load(GOLDEN / "backward_cases.npz")
+
+
+def _spec(case):
+    return ConvSpec(kernel=tuple(case["kernel"]), stride=tuple(case["stride"]), pad=tuple(case["pad"]))
+
+
+def _inputs(case):
+    k = case["name"]
+    return ARR[f"{k}/data"], ARR[f"{k}/weights"], ARR[f"{k}/grad_out"]
+
+
+# ---------------------------------------------------------------- CPU (oracle)
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_oracle_grads_match_reference_golden(case):
+    """Pins the oracle restatement against the reference's dwm_backward."""
+    d, g, dy = _inputs(case)
+    gd, gw = direct_conv2d_grads_f64(d, g, _spec(case), dy)
+    k = case["name"]
+    assert np.max(np.abs(gd - ARR[f"{k}/gd64"])) <= 1e-10
+    assert np.max(np.abs(gw - ARR[f"{k}/gw64"])) <= 1e-10
+
+
+def test_oracle_grads_match_reference_module(ref):
+    """Oracle vs the reference test-suite's literal-loop oracle_grads semantics
+    (reference.py:48-71) re-derived through the reference dwm_backward."""
+    rng = np.random.default_rng(5)
+    spec = ConvSpec(kernel=(4, 3), stride=(3, 2), pad=(2, 1, 0, 2))
+    d = rng.standard_normal((2, 3, 11, 10))
+    g = rng.standard_normal((2, 3, 4, 3))
+    rspec = ref.ConvSpec(kernel=(4, 3), stride=(3, 2), pad=(2, 1, 0, 2))
+    oh, ow = rspec.out_dims(11, 10)
+    dy = rng.standard_normal((2, 2, oh, ow))
+    from dwmconv.engines import dwm_backward as ref_backward
+    want_d, want_w = ref_backward(dy, ref.plan_decomposition(rspec), d, g)
+    got_d, got_w = direct_conv2d_grads_f64(d, g, spec, dy)
+    assert np.max(np.abs(got_d - want_d)) <= 1e-10
+    assert np.max(np.abs(got_w - want_w)) <= 1e-10
+
+
+def test_backward_rejects_bad_grad_shape():
+    """reference test_engines_backward.py:135-141 (raised before any device work)."""
+    spec = ConvSpec(kernel=(3, 3))
+    with pytest.raises(ValueError, match="grad_out"):
+        dwm_backward(np.zeros((1, 1, 2, 2)), plan_decomposition(spec),
+                     np.zeros((1, 1, 8, 8)), np.zeros((1, 1, 3, 3)))
+
+
+def test_backward_rejects_bad_taps_and_channels():
+    spec = ConvSpec(kernel=(3, 3))
+    plan = plan_decomposition(spec)
+    with pytest.raises(ValueError, match="taps"):
+        dwm_backward(np.zeros((1, 1, 6, 6)), plan, np.zeros((1, 1, 8, 8)), np.zeros((1, 1, 5, 5)))
+    with pytest.raises(ValueError, match="channel mismatch"):
+        dwm_backward(np.zeros((1, 1, 6, 6)), plan, np.zeros((1, 2, 8, 8)), np.zeros((1, 1, 3, 3)))
+    with pytest.raises(TypeError):
+        dwm_backward([[0.0]], plan, np.zeros((1, 1, 8, 8)), np.zeros((1, 1, 3, 3)))
+
+
+# ---------------------------------------------------------------- GPU
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_backward_f64_matches_reference(cuda, case):
+    d, g, dy = _inputs(case)
+    spec = _spec(case)
+    gd, gw = dwm_backward(dy, plan_decomposition(spec), d, g)
+    assert gd.dtype == np.float64 and gd.shape == d.shape and gw.shape == g.shape
+    k = case["name"]
+    want_d, want_w = direct_conv2d_grads_f64(d, g, spec, dy)
+    assert np.max(np.abs(gd - want_d)) <= 1e-10
+    assert np.max(np.abs(gw - want_w)) <= 1e-10
+    assert np.max(np.abs(gd - ARR[f"{k}/gd64"])) <= 1e-10
+    assert np.max(np.abs(gw - ARR[f"{k}/gw64"])) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_backward_f32_error_at_reference_level(cuda, case):
+    d, g, dy = _inputs(case)
+    spec = _spec(case)
+    gd, gw = dwm_backward(dy, plan_decomposition(spec), d, g, precision=np.float32)
+    assert gd.dtype == np.float32 and gw.dtype == np.float32
+    k = case["name"]
+    want_d, want_w = ARR[f"{k}/gd64"], ARR[f"{k}/gw64"]
+    assert mse(gd, want_d) <= 4 * mse(ARR[f"{k}/gd32"], want_d) + 1e-14
+    assert mse(gw, want_w) <= 4 * mse(ARR[f"{k}/gw32"], want_w) + 1e-14
+
+
+@pytest.mark.gpu
+def test_backward_zero_grad_out(cuda):
+    """reference test_engines_backward.py:12-27"""
+    spec = ConvSpec(kernel=(5, 5), stride=(2, 2))
+    d = np.ones((1, 1, 9, 9))
+    w = np.ones((1, 1, 5, 5))
+    oh, ow = spec.out_dims(9, 9)
+    gd, gw = dwm_backward(np.zeros((1, 1, oh, ow)), plan_decomposition(spec), d, w)
+    np.testing.assert_array_equal(gd, np.zeros_like(d))
+    np.testing.assert_array_equal(gw, np.zeros_like(w))
+
+
+@pytest.mark.gpu
+def test_backward_ones_counts_windows(cuda):
+    """reference test_engines_backward.py:44-50 through dwm_backward: every
+    3x3 tap of a 4x4 all-ones input is covered by all four outputs."""
+    spec = ConvSpec(kernel=(3, 3))
+    gd, gw = dwm_backward(np.ones((1, 1, 2, 2)), plan_decomposition(spec),
+                          np.ones((1, 1, 4, 4)), np.ones((1, 1, 3, 3)))
+    np.testing.assert_array_equal(gw, np.full((1, 1, 3, 3), 4.0))
+
+
+@pytest.mark.gpu
+def test_backward_torch_io_and_determinism(cuda):
+    import torch
+    case = next(c for c in CASES if c["name"] == "bw_extra6")
+    d, g, dy = _inputs(case)
+    plan = plan_decomposition(_spec(case))
+    t = [torch.from_numpy(a).float().to(cuda) for a in (dy, d, g)]
+    gd1, gw1 = dwm_backward(t[0], plan, t[1], t[2])
+    gd2, gw2 = dwm_backward(t[0], plan, t[1], t[2])
+    assert gd1.is_cuda and gd1.dtype == torch.float32
+    assert torch.equal(gd1, gd2) and torch.equal(gw1, gw2)
+    gd_np, gw_np = dwm_backward(dy.astype(np.float32), plan, d.astype(np.float32), g.astype(np.float32))
+    assert np.array_equal(gd1.cpu().numpy(), gd_np) and np.array_equal(gw1.cpu().numpy(), gw_np)
+
+
+@pytest.mark.gpu
+def test_backward_nonfinite_raises(cuda):
+    spec = ConvSpec(kernel=(3, 3))
+    d = np.ones((1, 1, 6, 6))
+    d[0, 0, 2, 2] = np.inf
+    with pytest.raises(FloatingPointError, match="dwm_backward"):
+        dwm_backward(np.ones((1, 1, 4, 4)), plan_decomposition(spec), d, np.ones((1, 1, 3, 3)))
