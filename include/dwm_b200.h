@@ -138,10 +138,14 @@ int dwm_conv2d_forward_prepared(const dwm_desc_t* desc, int dtype, int algo, con
 
 /* Weight gradient of the forward (reference
  * dwm_backward, engines.py:342-399): gw[F,C,r_h,r_w] from x[N,C,H,W] and
- * dy[N,F,OH,OW]; deterministic fixed-order reduction.  (The data gradient is
- * computed by the forward engine on the adjoint problem, see engines.py.) */
+ * dy[N,F,OH,OW] as an implicit-im2col GEMM over (n, oy, ox) with a split-K
+ * whose split count depends only on the geometry, partials summed in fixed
+ * order: deterministic.  workspace >= dwm_weight_grad_workspace_bytes (may be
+ * 0 -> NULL allowed).  (The data gradient is computed by the forward engine on
+ * the adjoint problem, see engines.py.) */
+size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* desc, int dtype);
 int dwm_weight_grad(const dwm_desc_t* desc, int dtype, const void* x, const void* dy,
-                    void* gw, void* stream);
+                    void* gw, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Whole forward: y[N,F,OH,OW] = dwm_conv2d(x[N,C,H,W], w[F,C,r_h,r_w]).
  * nonfinite_flag (device int32, may be NULL) is set to 1 when any output

@@ -173,9 +173,17 @@ int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, con
   return launch_gemm_exact(*d, dtype, V, U, y, flag, (cudaStream_t)stream);
 }
 
-int dwm_weight_grad(const dwm_desc_t* d, int dtype, const void* x, const void* dy, void* gw, void* stream) {
+size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* d, int dtype) {
+  if (!d || d->num_freqs <= 0) return 0;
+  const int splits = weight_grad_splits(*d);
+  if (splits <= 1) return 0;
+  return (size_t)splits * d->f * d->c * d->r_h * d->r_w * (dtype == DWM_F64 ? 8 : 4);
+}
+
+int dwm_weight_grad(const dwm_desc_t* d, int dtype, const void* x, const void* dy, void* gw, void* ws,
+                    size_t ws_bytes, void* stream) {
   if (int st = check_common(d, dtype)) return st;
-  return launch_weight_grad(*d, dtype, x, dy, gw, (cudaStream_t)stream);
+  return launch_weight_grad(*d, dtype, x, dy, gw, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int dwm_conv2d_small_c(const dwm_desc_t* d, const void* x, const void* U, void* y, int32_t* flag,

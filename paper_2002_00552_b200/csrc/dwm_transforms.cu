@@ -12,6 +12,7 @@
 #include "dwm_kernels.h"
 #include "dwm_wino.cuh"
 
+#include <algorithm>
 #include <cstring>
 
 namespace dwm {
@@ -374,61 +375,181 @@ int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* 
 namespace dwm {
 
 // ---------------------------------------------------------------------------
-// Weight gradient: dW[f,c,ky,kx] = sum_{n,oy,ox}
-// dY[n,f,oy,ox] * x_pad[n,c,s_h*oy+ky,s_w*ox+kx].  One warp per (f, c, ky):
-// lanes stride over (n, oy, ox) in a fixed order, kx taps in registers, then a
-// fixed-order warp-shuffle reduction -- deterministic run to run.
+// Weight gradient: the GEMM
+//   gw[f][j] = sum_p dY[f][p] * X[j][p],  j = (c, ky, kx),  p = (n, oy, ox),
+// X gathered on the fly from x (implicit im2col; padding by predicate).
+// 64x64 output tile per CTA, 256 threads x (4 filters x 4 taps), K chunks of
+// 16 positions through smem.  Each output is one FMA chain in ascending p, so
+// results are deterministic and independent of the launch configuration.
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) weight_grad_kernel(const dwm_desc_t d, const T* __restrict__ x,
-                                                          const T* __restrict__ dy, T* __restrict__ gw) {
-  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  const int64_t nw = (int64_t)d.f * d.c * d.r_h;
-  if (wid >= nw) return;
-  const int ky = (int)(wid % d.r_h);
-  const int c = (int)((wid / d.r_h) % d.c);
-  const int f = (int)(wid / ((int64_t)d.r_h * d.c));
-  constexpr int MAXR = 16;
-  T acc[MAXR];
-#pragma unroll
-  for (int k = 0; k < MAXR; ++k) acc[k] = T(0);
+                                                          const T* __restrict__ dy, T* __restrict__ gw,
+                                                          int64_t seg_len) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ __align__(16) T As[BK][BM];
+  __shared__ __align__(16) T Bs[BK][BN];
+  __shared__ int p_img[BK], p_oy[BK], p_ox[BK];
+  const int tid = threadIdx.x;
+  const int taps = d.r_h * d.r_w;
+  const int ncols = d.c * taps;
+  const int f0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
   const int64_t per_img = (int64_t)d.oh * d.ow;
-  const int64_t total = (int64_t)d.n * per_img;
-  for (int64_t e = lane; e < total; e += 32) {
-    const int n = (int)(e / per_img);
-    const int rem = (int)(e % per_img);
-    const int oy = rem / d.ow, ox = rem % d.ow;
-    const T g = dy[(((int64_t)n * d.f + f) * d.oh + oy) * d.ow + ox];
-    const int row = d.s_h * oy + ky - d.pad_top;
-    if (row < 0 || row >= d.h) continue;
-    const T* xr = x + (((int64_t)n * d.c + c) * d.h + row) * d.w;
-    const int col0 = d.s_w * ox - d.pad_left;
+  // K segment blockIdx.z (split-K; partial sums go to gw + z * F * ncols)
+  const int64_t k_begin = (int64_t)blockIdx.z * seg_len;
+  const int64_t K = min((int64_t)d.n * per_img, k_begin + seg_len);
+  gw += (int64_t)blockIdx.z * d.f * ncols;
+
+  // this thread's fixed X column (tap) for the gather: j = j0 + tid % 64
+  const int jl = tid % BN;
+  const int jg = j0 + jl;
+  const bool j_ok = jg < ncols;
+  const int jc = j_ok ? jg / taps : 0;
+  const int jky = j_ok ? (jg % taps) / d.r_w : 0;
+  const int jkx = j_ok ? jg % d.r_w : 0;
+  const int kk = tid / BN;  // rows kk, kk+4, kk+8, kk+12 of the K chunk
+
+  // dY loads: k fastest (coalesced along ox), filters tid/16 + 16 i
+  const int ak = tid % BK;
+  const int af = tid / BK;
+
+  const int ty = tid / 16, tx = tid % 16;
+  // blocked summation (like a BLAS kernel): 16-position chunk sums -> 1024-
+  // position block sums -> total; error grows with ~K/1024 + 64 + 16 terms
+  // instead of K for one long chain
+  T acc[4][4], mid[4][4], tot[4][4];
 #pragma unroll
-    for (int kx = 0; kx < MAXR; ++kx) {
-      if (kx >= d.r_w) break;
-      const int col = col0 + kx;
-      if (col >= 0 && col < d.w) acc[kx] = fma_rn(g, xr[col], acc[kx]);
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) mid[a][b] = tot[a][b] = T(0);
+  int chunk = 0;
+
+  for (int64_t k0 = k_begin; k0 < K; k0 += BK) {
+    if (tid < BK) {
+      const int64_t p = k0 + tid;
+      if (p < K) {
+        p_img[tid] = (int)(p / per_img);
+        const int rem = (int)(p % per_img);
+        p_oy[tid] = rem / d.ow;
+        p_ox[tid] = rem % d.ow;
+      } else {
+        p_img[tid] = -1;
+      }
     }
+    __syncthreads();
+    {
+      const int n = p_img[ak];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int f = f0 + af + 16 * i;
+        T v = T(0);
+        if (n >= 0 && f < d.f) v = dy[(((int64_t)n * d.f + f) * d.oh + p_oy[ak]) * d.ow + p_ox[ak]];
+        As[ak][af + 16 * i] = v;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = kk + 4 * i;
+        const int nn = p_img[k];
+        T v = T(0);
+        if (nn >= 0 && j_ok) {
+          const int row = d.s_h * p_oy[k] + jky - d.pad_top;
+          const int col = d.s_w * p_ox[k] + jkx - d.pad_left;
+          if (row >= 0 && row < d.h && col >= 0 && col < d.w)
+            v = x[(((int64_t)nn * d.c + jc) * d.h + row) * d.w + col];
+        }
+        Bs[k][jl] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = T(0);
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      T a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = As[k][ty * 4 + q];
+        b[q] = Bs[k][tx * 4 + q];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma_rn(a[u], b[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) mid[u][v] = add_rn(mid[u][v], acc[u][v]);
+    if (++chunk == 64) {
+      chunk = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          tot[u][v] = add_rn(tot[u][v], mid[u][v]);
+          mid[u][v] = T(0);
+        }
+    }
+    __syncthreads();
   }
 #pragma unroll
-  for (int kx = 0; kx < MAXR; ++kx) {
-    if (kx >= d.r_w) break;
-    T v = acc[kx];
+  for (int u = 0; u < 4; ++u) {
+    const int f = f0 + ty * 4 + u;
+    if (f >= d.f) continue;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = add_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-    if (lane == 0) gw[((((int64_t)f * d.c + c) * d.r_h) + ky) * d.r_w + kx] = v;
+    for (int v = 0; v < 4; ++v) {
+      const int j = j0 + tx * 4 + v;
+      if (j < ncols) gw[(int64_t)f * ncols + j] = add_rn(tot[u][v], mid[u][v]);
+    }
   }
 }
 
-int launch_weight_grad(const dwm_desc_t& d, int dtype, const void* x, const void* dy, void* gw, cudaStream_t s) {
-  if (d.r_w > 16) return fail(DWM_EUNSUPPORTED, "weight gradient kernel supports r_w <= 16, got %d", d.r_w);
-  const int64_t warps = (int64_t)d.f * d.c * d.r_h;
-  const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
-  if (dtype == DWM_F64)
-    weight_grad_kernel<double><<<grid, 256, 0, s>>>(d, (const double*)x, (const double*)dy, (double*)gw);
-  else
-    weight_grad_kernel<float><<<grid, 256, 0, s>>>(d, (const float*)x, (const float*)dy, (float*)gw);
+// Fixed-order sum of the split-K partials (segment 0 first).
+template <typename T>
+__global__ void weight_grad_reduce_kernel(const T* __restrict__ part, T* __restrict__ gw, int64_t count,
+                                          int splits) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  T v = part[i];
+  for (int z = 1; z < splits; ++z) v = add_rn(v, part[(int64_t)z * count + i]);
+  gw[i] = v;
+}
+
+// Split count from the geometry only (never from the device), so a given
+// problem always sums in the same order: enough CTAs for ~2 waves of 148 SMs,
+// segments of at least 4096 positions.
+int weight_grad_splits(const dwm_desc_t& d) {
+  const int64_t ncols = (int64_t)d.c * d.r_h * d.r_w;
+  const int64_t tiles = ((ncols + 63) / 64) * ((d.f + 63) / 64);
+  const int64_t K = (int64_t)d.n * d.oh * d.ow;
+  int64_t sp = (2 * 148 + tiles - 1) / tiles;
+  sp = std::min<int64_t>(sp, (K + 4095) / 4096);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(sp, 256));
+}
+
+int launch_weight_grad(const dwm_desc_t& d, int dtype, const void* x, const void* dy, void* gw, void* ws,
+                       size_t ws_bytes, cudaStream_t s) {
+  const int ncols = d.c * d.r_h * d.r_w;
+  const int splits = weight_grad_splits(d);
+  const int64_t K = (int64_t)d.n * d.oh * d.ow;
+  const int64_t seg = ((K + splits - 1) / splits + 15) / 16 * 16;
+  const int64_t count = (int64_t)d.f * ncols;
+  const size_t es = dtype == DWM_F64 ? 8 : 4;
+  if (splits > 1 && (!ws || ws_bytes < (size_t)splits * count * es))
+    return fail(DWM_EINVAL_SHAPE, "weight-gradient workspace too small: %zu bytes given, %zu needed", ws_bytes,
+                (size_t)splits * count * es);
+  const dim3 grid((unsigned)((ncols + 63) / 64), (unsigned)((d.f + 63) / 64), (unsigned)splits);
+  void* dst = splits > 1 ? ws : gw;
+  const unsigned rg = (unsigned)((count + 255) / 256);
+  if (dtype == DWM_F64) {
+    weight_grad_kernel<double><<<grid, 256, 0, s>>>(d, (const double*)x, (const double*)dy, (double*)dst, seg);
+    if (splits > 1) weight_grad_reduce_kernel<double><<<rg, 256, 0, s>>>((const double*)ws, (double*)gw, count, splits);
+  } else {
+    weight_grad_kernel<float><<<grid, 256, 0, s>>>(d, (const float*)x, (const float*)dy, (float*)dst, seg);
+    if (splits > 1) weight_grad_reduce_kernel<float><<<rg, 256, 0, s>>>((const float*)ws, (float*)gw, count, splits);
+  }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }

@@ -252,25 +252,77 @@ def _to_device(x, dev, tdt):
     return t.to(dev, dtype=tdt).contiguous()
 
 
+def _phase_geometry(rho: int, s: int, r: int, pad_lo: int, size: int, out: int):
+    """One axis of input-gradient phase rho (positions p = s*i + rho of the
+    padded input).  Taps with k = rho (mod s) reach it: T = ceil((r-rho)/s).
+    Returns (T, i_min, m, pad_lo', pad_hi') for the stride-1 correlation of
+    grad_out with the reversed sub-kernel that yields rows i_min .. i_min+m-1
+    (negative pads mean cropping grad_out)."""
+    taps = max(0, -(-(r - rho) // s))
+    i_min = -(-(pad_lo - rho) // s)
+    i_max = (pad_lo + size - 1 - rho) // s
+    m = i_max - i_min + 1
+    lo = taps - 1 - i_min
+    hi = m - 1 + taps - out - lo
+    return taps, i_min, m, lo, hi
+
+
+def _data_grad_polyphase(dy, wt, spec: ConvSpec, hw, algo: str, stream):
+    """Input gradient as s_h*s_w stride-1 DWM forwards (one per output phase):
+    grad_pad[s*i + rho] = sum_t dY[i - t] * w[rho + s*t]  -- the DWM stride
+    split applied to the adjoint, so no zero-inserted (dilated) grad_out and no
+    multiply by an inserted zero.  Phases write disjoint positions."""
+    torch = _torch()
+    n, f, oh, ow = dy.shape
+    c = wt.shape[1]
+    h, w = hw
+    r_h, r_w = spec.kernel
+    s_h, s_w = spec.stride
+    top, _, left, _ = spec.pad
+    rows = [_phase_geometry(rho, s_h, r_h, top, h, oh) for rho in range(s_h)]
+    cols = [_phase_geometry(sig, s_w, r_w, left, w, ow) for sig in range(s_w)]
+    covered = all(g[0] > 0 for g in rows + cols)
+    gd = (torch.empty if covered else torch.zeros)((n, c, h, w), dtype=dy.dtype, device=dy.device)
+    w_t = wt.transpose(0, 1)  # (C, F, r_h, r_w)
+    for rho, (tr, i0, m, pt, pb) in enumerate(rows):
+        if tr == 0 or m <= 0:
+            continue
+        for sig, (tc, j0, mc, pl, pr) in enumerate(cols):
+            if tc == 0 or mc <= 0:
+                continue
+            sub = w_t[:, :, rho::s_h, sig::s_w].flip(2, 3).contiguous()  # (C, F, tr, tc)
+            src = dy
+            if min(pt, pb, pl, pr) < 0:
+                src = dy[:, :, max(0, -pt):oh - max(0, -pb), max(0, -pl):ow - max(0, -pr)]
+            adj = ConvSpec(kernel=(tr, tc), stride=(1, 1),
+                           pad=(max(0, pt), max(0, pb), max(0, pl), max(0, pr)))
+            y = dwm_conv2d(src.contiguous(), sub, adj, algo=algo, check_finite=False, stream=stream)
+            r0, c0 = s_h * i0 + rho - top, s_w * j0 + sig - left
+            gd[:, :, r0::s_h, c0::s_w] = y
+    return gd
+
+
 def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=None, *,
-                 algo: str = "auto", stream=None):
+                 algo: str = "auto", stream=None, need_data: bool = True, need_weights: bool = True):
     """Gradients of ``dwm_conv2d`` w.r.t. data and weights on B200 (SURVEY §8f
     rank 1; reference ``engines.py:342-399``, same signature, checks and
     messages).  Returns ``(grad_data, grad_weights)``.
 
     B200 design (not the reference's per-part Winograd adjoint):
 
-    * data gradient -- the adjoint of a stride-s correlation is a stride-1
-      correlation of the s-dilated ``grad_out`` with the 180-degree-rotated,
-      channel-transposed kernel.  That is itself a DWM forward, so it runs on
-      the forward engine (tcgen05 3xTF32 when the channel counts allow);
-      padding of the adjoint problem is ``r-1-pad`` (negative -> crop).
-    * weight gradient -- ``dwm_weight_grad`` (C ABI): a deterministic
-      fixed-order reduction over (image, output row, output column) per
-      (filter, channel, tap row) warp.
+    * data gradient -- the adjoint of a stride-s correlation splits, by the
+      same stride decomposition DWM uses, into s_h*s_w stride-1 correlations
+      of ``grad_out`` with reversed, channel-transposed sub-kernels
+      w[:, :, rho::s, sig::s], one per phase of the input gradient.  Each is
+      a DWM forward, so it runs on the forward engines (tcgen05 3xTF32 when
+      the channel counts allow) with no zero-inserted grad_out.
+    * weight gradient -- ``dwm_weight_grad`` (C ABI): an implicit-im2col
+      GEMM over (image, output row, output column) with a geometry-fixed
+      split-K and a fixed-order partial sum (deterministic).
 
     Both are exact in exact arithmetic, so results agree with the reference's
     to rounding (binary64: <= 1e-10 absolute, the reference's own criterion).
+    ``need_data`` / ``need_weights`` = False skip a gradient (returned as None).
     """
     _check_pair(data, weights)
     _require_tensor4(grad_out, "grad_out")
@@ -293,8 +345,6 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
     cuda_in = _is_torch(grad_out) and grad_out.is_cuda
     dev = grad_out.device if cuda_in else torch.device("cuda", torch.cuda.current_device())
     r_h, r_w = spec.kernel
-    s_h, s_w = spec.stride
-    top, _, left, _ = spec.pad
 
     with torch.cuda.device(dev):
         s = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -303,32 +353,23 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
             x = _to_device(data, dev, tdt)
             wt = _to_device(weights, dev, tdt)
 
-            gw = torch.empty((f, c, r_h, r_w), dtype=tdt, device=dev)
-            desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
-            _native.check(lib.dwm_weight_grad(desc, code, x.data_ptr(), dy.data_ptr(), gw.data_ptr(),
-                                              s.cuda_stream), "dwm_weight_grad")
-
-            hd, wd = s_h * (oh - 1) + 1, s_w * (ow - 1) + 1
-            if (s_h, s_w) != (1, 1):
-                dil = torch.zeros((n, f, hd, wd), dtype=tdt, device=dev)
-                dil[:, :, ::s_h, ::s_w] = dy
-            else:
-                dil = dy
-            pt, pb = r_h - 1 - top, h + top - hd
-            pl, pr = r_w - 1 - left, w + left - wd
-            if min(pt, pb, pl, pr) < 0:
-                dil = dil[:, :, max(0, -pt):dil.shape[2] - max(0, -pb),
-                          max(0, -pl):dil.shape[3] - max(0, -pr)]
-                pt, pb, pl, pr = (max(0, p) for p in (pt, pb, pl, pr))
-            w_adj = wt.flip(2, 3).transpose(0, 1).contiguous()
-            adj = ConvSpec(kernel=spec.kernel, stride=(1, 1), pad=(pt, pb, pl, pr))
-            gd = dwm_conv2d(dil.contiguous(), w_adj, adj, algo=algo, check_finite=False, stream=s)
-            if not (bool(torch.isfinite(gd).all()) and bool(torch.isfinite(gw).all())):
-                raise FloatingPointError("dwm_backward produced non-finite values")
+            gw = None
+            if need_weights:
+                gw = torch.empty((f, c, r_h, r_w), dtype=tdt, device=dev)
+                desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+                wg_bytes = int(lib.dwm_weight_grad_workspace_bytes(desc, code))
+                wg_ws = torch.empty(max(wg_bytes, 1), dtype=torch.uint8, device=dev)
+                _native.check(lib.dwm_weight_grad(desc, code, x.data_ptr(), dy.data_ptr(), gw.data_ptr(),
+                                                  wg_ws.data_ptr(), wg_bytes, s.cuda_stream),
+                              "dwm_weight_grad")
+            gd = _data_grad_polyphase(dy, wt, spec, (h, w), algo, s) if need_data else None
+            for g in (gd, gw):
+                if g is not None and not bool(torch.isfinite(g).all()):
+                    raise FloatingPointError("dwm_backward produced non-finite values")
     if not _is_torch(grad_out):
-        return gd.cpu().numpy(), gw.cpu().numpy()
+        return tuple(None if g is None else g.cpu().numpy() for g in (gd, gw))
     if not cuda_in:
-        return gd.cpu(), gw.cpu()
+        return tuple(None if g is None else g.cpu() for g in (gd, gw))
     return gd, gw
 
 

@@ -124,9 +124,9 @@ class DWMConv2dFunction(torch.autograd.Function):
     def backward(ctx, grad_y):
         x, w = ctx.saved_tensors
         gd, gw = dwm_backward(grad_y.contiguous(), ctx.plan, x.contiguous(), w.contiguous(),
-                              algo=ctx.algo)
-        return (gd if ctx.needs_input_grad[0] else None, gw if ctx.needs_input_grad[1] else None,
-                None, None, None, None, None)
+                              algo=ctx.algo, need_data=ctx.needs_input_grad[0],
+                              need_weights=ctx.needs_input_grad[1])
+        return gd, gw, None, None, None, None, None
 
 
 def dwm_conv2d_op(x: torch.Tensor, w: torch.Tensor, spec: ConvSpec, plan: DecompositionPlan = None,

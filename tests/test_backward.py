@@ -157,3 +157,27 @@ def test_backward_nonfinite_raises(cuda):
     d[0, 0, 2, 2] = np.inf
     with pytest.raises(FloatingPointError, match="dwm_backward"):
         dwm_backward(np.ones((1, 1, 4, 4)), plan_decomposition(spec), d, np.ones((1, 1, 3, 3)))
+
+
+@pytest.mark.gpu
+def test_backward_need_flags(cuda):
+    case = next(c for c in CASES if c["name"] == "bw_r7_s2")
+    d, g, dy = _inputs(case)
+    plan = plan_decomposition(_spec(case))
+    gd_all, gw_all = dwm_backward(dy, plan, d, g)
+    gd, gw = dwm_backward(dy, plan, d, g, need_weights=False)
+    assert gw is None and np.array_equal(gd, gd_all)
+    gd, gw = dwm_backward(dy, plan, d, g, need_data=False)
+    assert gd is None and np.array_equal(gw, gw_all)
+
+
+@pytest.mark.gpu
+def test_backward_batch_invariance(cuda):
+    """Per-image data gradients do not depend on the batch they are in."""
+    case = next(c for c in CASES if c["name"] == "bw_extra6")
+    d, g, dy = _inputs(case)
+    plan = plan_decomposition(_spec(case))
+    gd, _ = dwm_backward(dy, plan, d, g, need_weights=False)
+    for i in range(d.shape[0]):
+        gdi, _ = dwm_backward(dy[i:i + 1], plan, d[i:i + 1], g, need_weights=False)
+        assert np.array_equal(gd[i:i + 1], gdi)
