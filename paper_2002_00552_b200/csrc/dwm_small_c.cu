@@ -32,6 +32,8 @@
 #include <utility>
 
 #include "dwm_common.cuh"
+#include <cstdlib>
+#include <cstring>
 #include "dwm_kernels.h"
 #include "dwm_wino.cuh"
 
@@ -83,9 +85,9 @@ template <int K, bool FIRST> __device__ __forceinline__ void chain2(f2& acc, f2 
   else acc = sub2(acc, m);
 }
 
-template <int CC_, int TM_, int TN_>
+template <int CC_, int TM_, int TN_, int MINB_ = 1>
 struct Cfg {
-  static constexpr int CC = CC_, TM = TM_, TN = TN_;
+  static constexpr int CC = CC_, TM = TM_, TN = TN_, MINB = MINB_;
   static constexpr int BM = 32 * TM;         // tiles per block
   static constexpr int BN = 8 * TN;          // filters per block
   static constexpr int NP = TN / 2;          // filter pairs per thread
@@ -223,7 +225,7 @@ __device__ __forceinline__ void transform_store(const float (&win)[4][4], float*
 }
 
 template <class K>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, K::MINB)
 small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __restrict__ U,
                float* __restrict__ y, int32_t* __restrict__ flag) {
   constexpr int CC = K::CC, BM = K::BM, BN = K::BN, TM = K::TM, TN = K::TN, NP = K::NP;
@@ -377,12 +379,25 @@ int launch_cfg(const dwm_desc_t& d, const float* x, const float* U, float* y, in
 constexpr size_t SMEM_CAP = 220 * 1024;
 
 // Wide variant (2 tiles x 8 filters per thread, 64x64 block) when its resident
-// U fits; else the narrow one (4 tiles x 4 filters, 128x32 block).
+// U fits; else Tall (1 x 8, 32x64 block); else Narrow (4 x 4, 128x32 block).
+// (Measured on cfg2/cfg3 against 2x4, 1x4, 1x8 with 2 CTAs/SM: see DESIGN.md.)
 template <int CC>
 int launch_cc(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
   using Wide = Cfg<CC, 2, 8>;
   using Narrow = Cfg<CC, 4, 4>;
+  if (const char* e = getenv("DWM_SC_CFG")) {  // tuning experiments only
+    if (!strcmp(e, "2x4x2")) return launch_cfg<Cfg<CC, 2, 4, 2>>(d, x, U, y, flag, s);
+    if (!strcmp(e, "2x4x1")) return launch_cfg<Cfg<CC, 2, 4, 1>>(d, x, U, y, flag, s);
+    if (!strcmp(e, "1x8x2")) return launch_cfg<Cfg<CC, 1, 8, 2>>(d, x, U, y, flag, s);
+    if (!strcmp(e, "2x8x1")) return launch_cfg<Cfg<CC, 2, 8, 1>>(d, x, U, y, flag, s);
+    if (!strcmp(e, "1x8x1")) return launch_cfg<Cfg<CC, 1, 8, 1>>(d, x, U, y, flag, s);
+    if (!strcmp(e, "1x4x2")) return launch_cfg<Cfg<CC, 1, 4, 2>>(d, x, U, y, flag, s);
+  }
+  using Tall = Cfg<CC, 1, 8>;
   if (d.f > 32 && Wide::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_cfg<Wide>(d, x, U, y, flag, s);
+  // many frequencies (e.g. 11x11/4: 225): keep 64 filters per block -- one V
+  // transform feeds twice the filters -- with a 32-tile block (cfg3: 1.34x)
+  if (d.f > 32 && Tall::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_cfg<Tall>(d, x, U, y, flag, s);
   return launch_cfg<Narrow>(d, x, U, y, flag, s);
 }
 
