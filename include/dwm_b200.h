@@ -137,14 +137,20 @@ int dwm_conv2d_forward_prepared(const dwm_desc_t* desc, int dtype, int algo, con
                                 int32_t* nonfinite_flag, void* stream);
 
 /* Weight gradient of the forward (reference
- * dwm_backward, engines.py:342-399): gw[F,C,r_h,r_w] from x[N,C,H,W] and
- * dy[N,F,OH,OW] as an implicit-im2col GEMM over (n, oy, ox) with a split-K
- * whose split count depends only on the geometry, partials summed in fixed
- * order: deterministic.  workspace >= dwm_weight_grad_workspace_bytes (may be
- * 0 -> NULL allowed).  (The data gradient is computed by the forward engine on
- * the adjoint problem, see engines.py.) */
-size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* desc, int dtype);
-int dwm_weight_grad(const dwm_desc_t* desc, int dtype, const void* x, const void* dy,
+ * dwm_backward / _winograd_grad_weight_impl, engines.py:258-330,342-399):
+ * gw[F,C,r_h,r_w] from x[N,C,H,W] and dy[N,F,OH,OW].  Engines (`algo`):
+ *   DWM_ALGO_TC    (AUTO's choice for float32, C % 32 == 0, C >= 64, F >= 64):
+ *                  Winograd domain like the reference -- V = B^T x B (the
+ *                  forward's input transform), DM = A dY A^T, per frequency
+ *                  dU = V^T DM on tcgen05 (3xTF32, K = tiles, blocked FP32
+ *                  sums), then G^T dU G placed at each part's taps;
+ *   DWM_ALGO_EXACT (any shape, float64): implicit-im2col GEMM on CUDA cores,
+ *                  geometry-fixed split-K, fixed-order partial sums.
+ * Both deterministic.  workspace >= dwm_weight_grad_workspace_bytes (may be
+ * 0 -> NULL allowed).  (The data gradient is computed by the forward engines
+ * on the polyphase adjoint problems, see engines.py.) */
+size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* desc, int dtype, int algo);
+int dwm_weight_grad(const dwm_desc_t* desc, int dtype, int algo, const void* x, const void* dy,
                     void* gw, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Whole forward: y[N,F,OH,OW] = dwm_conv2d(x[N,C,H,W], w[F,C,r_h,r_w]).

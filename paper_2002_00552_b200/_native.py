@@ -100,9 +100,9 @@ def load(required: bool = True):
     lib.dwm_prepare_filter.restype = I
     lib.dwm_conv2d_forward_prepared.argtypes = [D, I, I, P, P, P, P, ctypes.c_size_t, P, P]
     lib.dwm_conv2d_forward_prepared.restype = I
-    lib.dwm_weight_grad_workspace_bytes.argtypes = [D, I]
+    lib.dwm_weight_grad_workspace_bytes.argtypes = [D, I, I]
     lib.dwm_weight_grad_workspace_bytes.restype = S
-    lib.dwm_weight_grad.argtypes = [D, I, P, P, P, P, S, P]
+    lib.dwm_weight_grad.argtypes = [D, I, I, P, P, P, P, S, P]
     lib.dwm_weight_grad.restype = I
     lib.dwm_conv2d_small_c.argtypes = [D, P, P, P, P, P]
     lib.dwm_conv2d_small_c.restype = I

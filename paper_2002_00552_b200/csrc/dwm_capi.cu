@@ -173,16 +173,33 @@ int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, con
   return launch_gemm_exact(*d, dtype, V, U, y, flag, (cudaStream_t)stream);
 }
 
-size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* d, int dtype) {
+static int wgrad_select(const dwm_desc_t* d, int dtype, int algo) {
+  const bool tc_ok = dtype == DWM_F32 && wgrad_tc_supported(*d);
+  switch (algo) {
+    case DWM_ALGO_AUTO: return tc_ok ? DWM_ALGO_TC : DWM_ALGO_EXACT;
+    case DWM_ALGO_EXACT: return DWM_ALGO_EXACT;
+    case DWM_ALGO_TC: return tc_ok ? DWM_ALGO_TC : -1;
+    default: return -1;
+  }
+}
+
+size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* d, int dtype, int algo) {
   if (!d || d->num_freqs <= 0) return 0;
+  const int sel = wgrad_select(d, dtype, algo);
+  if (sel == DWM_ALGO_TC) return wgrad_tc_workspace_bytes(*d);
   const int splits = weight_grad_splits(*d);
   if (splits <= 1) return 0;
   return (size_t)splits * d->f * d->c * d->r_h * d->r_w * (dtype == DWM_F64 ? 8 : 4);
 }
 
-int dwm_weight_grad(const dwm_desc_t* d, int dtype, const void* x, const void* dy, void* gw, void* ws,
+int dwm_weight_grad(const dwm_desc_t* d, int dtype, int algo, const void* x, const void* dy, void* gw, void* ws,
                     size_t ws_bytes, void* stream) {
   if (int st = check_common(d, dtype)) return st;
+  const int sel = wgrad_select(d, dtype, algo);
+  if (sel < 0)
+    return fail(DWM_EUNSUPPORTED, "weight-gradient engine %d not available (tcgen05: float32, C %% 32 == 0, "
+                "C >= 64, F >= 64; got C=%d F=%d)", algo, d->c, d->f);
+  if (sel == DWM_ALGO_TC) return launch_wgrad_tc(*d, x, dy, gw, ws, ws_bytes, (cudaStream_t)stream);
   return launch_weight_grad(*d, dtype, x, dy, gw, ws, ws_bytes, (cudaStream_t)stream);
 }
 

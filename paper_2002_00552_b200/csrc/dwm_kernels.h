@@ -13,6 +13,10 @@ int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* 
 int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void* U, void* y,
                       int32_t* flag, cudaStream_t s);
 int weight_grad_splits(const dwm_desc_t& d);
+bool wgrad_tc_supported(const dwm_desc_t& d);
+size_t wgrad_tc_workspace_bytes(const dwm_desc_t& d);
+int launch_wgrad_tc(const dwm_desc_t& d, const void* x, const void* dy, void* gw, void* ws, size_t ws_bytes,
+                    cudaStream_t s);
 int launch_weight_grad(const dwm_desc_t& d, int dtype, const void* x, const void* dy, void* gw, void* ws,
                        size_t ws_bytes, cudaStream_t s);
 bool small_c_supported(const dwm_desc_t& d);

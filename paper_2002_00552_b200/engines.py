@@ -303,7 +303,8 @@ def _data_grad_polyphase(dy, wt, spec: ConvSpec, hw, algo: str, stream):
 
 
 def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=None, *,
-                 algo: str = "auto", stream=None, need_data: bool = True, need_weights: bool = True):
+                 algo: str = "auto", stream=None, need_data: bool = True, need_weights: bool = True,
+                 wgrad_algo: str = "auto"):
     """Gradients of ``dwm_conv2d`` w.r.t. data and weights on B200 (SURVEY §8f
     rank 1; reference ``engines.py:342-399``, same signature, checks and
     messages).  Returns ``(grad_data, grad_weights)``.
@@ -316,9 +317,12 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
       w[:, :, rho::s, sig::s], one per phase of the input gradient.  Each is
       a DWM forward, so it runs on the forward engines (tcgen05 3xTF32 when
       the channel counts allow) with no zero-inserted grad_out.
-    * weight gradient -- ``dwm_weight_grad`` (C ABI): an implicit-im2col
-      GEMM over (image, output row, output column) with a geometry-fixed
-      split-K and a fixed-order partial sum (deterministic).
+    * weight gradient -- ``dwm_weight_grad`` (C ABI), ``wgrad_algo``:
+      "tc" (AUTO for float32, C % 32 == 0, C, F >= 64) works in the Winograd
+      domain like the reference: per frequency dU = V^T DM on tcgen05
+      (3xTF32, K = tiles), then G^T dU G placed at each part's taps;
+      "exact" is an implicit-im2col CUDA-core GEMM with a geometry-fixed
+      split-K.  Both deterministic.
 
     Both are exact in exact arithmetic, so results agree with the reference's
     to rounding (binary64: <= 1e-10 absolute, the reference's own criterion).
@@ -357,10 +361,11 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
             if need_weights:
                 gw = torch.empty((f, c, r_h, r_w), dtype=tdt, device=dev)
                 desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
-                wg_bytes = int(lib.dwm_weight_grad_workspace_bytes(desc, code))
-                wg_ws = torch.empty(max(wg_bytes, 1), dtype=torch.uint8, device=dev)
-                _native.check(lib.dwm_weight_grad(desc, code, x.data_ptr(), dy.data_ptr(), gw.data_ptr(),
-                                                  wg_ws.data_ptr(), wg_bytes, s.cuda_stream),
+                wg_algo = _native.ALGOS[wgrad_algo]
+                wg_bytes = int(lib.dwm_weight_grad_workspace_bytes(desc, code, wg_algo))
+                wg_ws = _workspace(dev, wg_bytes)
+                _native.check(lib.dwm_weight_grad(desc, code, wg_algo, x.data_ptr(), dy.data_ptr(),
+                                                  gw.data_ptr(), wg_ws.data_ptr(), wg_bytes, s.cuda_stream),
                               "dwm_weight_grad")
             gd = _data_grad_polyphase(dy, wt, spec, (h, w), algo, s) if need_data else None
             for g in (gd, gw):

@@ -164,31 +164,40 @@ def backward_case_specs():
              ((1, 1), (3, 2), (0, 0, 0, 0), (1, 3, 9, 8), 2),
              ((7, 7), (2, 2), (3, 3, 3, 3), (2, 3, 20, 20), 64),   # ResNet stem shape, small
              ((3, 3), (1, 1), (1, 1, 1, 1), (1, 64, 10, 10), 64),  # tensor-core adjoint
-             ((5, 5), (1, 1), (2, 2, 2, 2), (1, 32, 9, 9), 128)]
+             ((5, 5), (1, 1), (2, 2, 2, 2), (1, 32, 9, 9), 128),
+             ((5, 5), (2, 2), (2, 2, 2, 2), (2, 64, 15, 15), 64),   # tcgen05 weight gradient
+             ((7, 7), (1, 1), (3, 3, 3, 3), (1, 64, 12, 12), 64)]
     for i, (k, s, p, shp, f) in enumerate(extra):
         cases.append(dict(name=f"bw_extra{i}", seed=900 + i, kernel=k, stride=s, pad=p, shape=shp, f=f))
     return cases
+
+
+def backward_inputs(case):
+    """Seeded inputs of a backward case (tests regenerate them the same way)."""
+    rng = np.random.default_rng(case["seed"])
+    n, c, h, w = case["shape"]
+    spec = ConvSpec(kernel=tuple(case["kernel"]), stride=tuple(case["stride"]), pad=tuple(case["pad"]))
+    d = rng.standard_normal((n, c, h, w))
+    g = rng.standard_normal((case["f"], c, *case["kernel"]))
+    oh, ow = spec.out_dims(h, w)
+    dy = rng.standard_normal((n, case["f"], oh, ow))
+    return spec, d, g, dy
 
 
 def backward_cases():
     arrays = {}
     meta = []
     for case in backward_case_specs():
-        rng = np.random.default_rng(case["seed"])
-        n, c, h, w = case["shape"]
-        spec = ConvSpec(kernel=case["kernel"], stride=case["stride"], pad=case["pad"])
-        d = rng.standard_normal((n, c, h, w))
-        g = rng.standard_normal((case["f"], c, *case["kernel"]))
-        oh, ow = spec.out_dims(h, w)
-        dy = rng.standard_normal((n, case["f"], oh, ow))
+        spec, d, g, dy = backward_inputs(case)
         plan = plan_decomposition(spec)
         key = case["name"]
-        arrays[f"{key}/data"] = d
-        arrays[f"{key}/weights"] = g
-        arrays[f"{key}/grad_out"] = dy
-        arrays[f"{key}/gd64"], arrays[f"{key}/gw64"] = dwm_backward(dy, plan, d, g, precision=np.float64)
-        arrays[f"{key}/gd32"], arrays[f"{key}/gw32"] = dwm_backward(dy, plan, d, g, precision=np.float32)
-        meta.append({k: (list(v) if isinstance(v, tuple) else v) for k, v in case.items()})
+        gd64, gw64 = dwm_backward(dy, plan, d, g, precision=np.float64)
+        gd32, gw32 = dwm_backward(dy, plan, d, g, precision=np.float32)
+        arrays[f"{key}/gd64"], arrays[f"{key}/gw64"] = gd64, gw64
+        m = {k: (list(v) if isinstance(v, tuple) else v) for k, v in case.items()}
+        m["ref_mse_gd32"], m["ref_mse_gw32"] = mse(gd32, gd64), mse(gw32, gw64)
+        m["input_sums"] = [float(d.sum()), float(g.sum()), float(dy.sum())]
+        meta.append(m)
     np.savez_compressed(HERE / "backward_cases.npz", **arrays)
     (HERE / "backward_cases.json").write_text(json.dumps(meta, indent=1))
 

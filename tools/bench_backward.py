@@ -23,6 +23,7 @@ def main():
     ap.add_argument("workloads", nargs="*", default=list(WORKLOADS))
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--wgrad-algo", default="auto", choices=("auto", "exact", "tc"))
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     lib = _native.load()
@@ -39,17 +40,19 @@ def main():
         dy = torch.randn(n, wl.c_out, oh, ow, device=dev, generator=g)
         desc = _native.make_desc(n, wl.c_in, wl.hw, wl.hw, wl.c_out, spec.kernel, spec.stride, spec.pad)
         gw = torch.empty_like(w)
-        wg_bytes = int(lib.dwm_weight_grad_workspace_bytes(desc, _native.DWM_F32))
+        wg_algo = _native.ALGOS[args.wgrad_algo]
+        wg_bytes = int(lib.dwm_weight_grad_workspace_bytes(desc, _native.DWM_F32, wg_algo))
         wg_ws = torch.empty(max(wg_bytes, 1), dtype=torch.uint8, device=dev)
 
         def wgrad():
-            _native.check(lib.dwm_weight_grad(desc, _native.DWM_F32, x.data_ptr(), dy.data_ptr(), gw.data_ptr(),
+            _native.check(lib.dwm_weight_grad(desc, _native.DWM_F32, wg_algo, x.data_ptr(), dy.data_ptr(),
+                                              gw.data_ptr(),
                                               wg_ws.data_ptr(), wg_bytes, torch.cuda.current_stream().cuda_stream))
 
         def full():
-            dwm_backward(dy, plan, x, w)
+            dwm_backward(dy, plan, x, w, wgrad_algo=args.wgrad_algo)
 
-        res = {"workload": name, "batch": n}
+        res = {"workload": name, "batch": n, "wgrad_algo": args.wgrad_algo}
         for label, fn in (("backward", full), ("weight_grad", wgrad)):
             fn()
             torch.cuda.synchronize()
