@@ -97,14 +97,20 @@ def _check_pair(data, weights):
 _WORKSPACE = {}
 
 
-def _workspace(device, nbytes: int):
-    """Grow-only per-device scratch for V and U (stream-ordered reuse)."""
+def _workspace(device, nbytes: int, stream=None):
+    """Grow-only per-device scratch for V and U (stream-ordered reuse).  When
+    the kernels using it run on a stream other than the allocating (current)
+    one, the buffer is recorded on that stream so torch's caching allocator
+    cannot hand it out again before that stream's work finishes (matters when
+    a later, larger request replaces it)."""
     torch = _torch()
     buf = _WORKSPACE.get(device)
     if buf is None or buf.numel() < nbytes:
         _WORKSPACE.pop(device, None)
         buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
         _WORKSPACE[device] = buf
+    if stream is not None and stream != torch.cuda.current_stream(device):
+        buf.record_stream(stream)
     return buf
 
 
@@ -179,7 +185,7 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
             x_d = data.to(dev, dtype=tdt).contiguous()
             y_d = out if out is not None else torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
             ws_bytes = lib.dwm_workspace_bytes(desc, code, algo_code)
-            ws = _workspace(dev, ws_bytes)
+            ws = _workspace(dev, ws_bytes, s)
             st = lib.dwm_conv2d_forward(desc, code, algo_code, x_d.data_ptr(), w_d.data_ptr(),
                                         y_d.data_ptr(), ws.data_ptr(), ws_bytes,
                                         flag.data_ptr() if flag is not None else None,
@@ -221,7 +227,7 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
     ws_bytes = max(lib.dwm_workspace_bytes(_native.make_desc(
         b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad), code, algo_code)
         for b0, b1 in zip(bounds, bounds[1:]))
-    ws = _workspace(dev, ws_bytes)
+    ws = _workspace(dev, ws_bytes, s)
     for b0, b1 in zip(bounds, bounds[1:]):
         with torch.cuda.stream(s_in):
             x_d[b0:b1].copy_(x_h[b0:b1], non_blocking=True)
