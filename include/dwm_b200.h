@@ -54,11 +54,11 @@ typedef enum dwm_dtype { DWM_F32 = 0, DWM_F64 = 1 } dwm_dtype;
  *            sum) over a V workspace.  Bit-identical to the reference where
  *            its BLAS accumulates sequentially (small C); f32 and f64.
  *   TC:      tcgen05/TMEM 3xTF32 GEMM with the output transform, part sum and
- *            tile interleave fused in the epilogue (f32 only, C % 32 == 0,
- *            F % 64 == 0).
+ *            tile interleave fused in the epilogue (f32 only, C % 32 == 0;
+ *            any F, in 64-filter blocks).
  *   SMALL_C: one fused kernel (input transform computed in shared memory,
  *            same arithmetic as EXACT, no V workspace); f32, C_in <= 4.
- *   AUTO:    SMALL_C for C_in <= 4, TC when eligible and C_in >= 64, else
+ *   AUTO:    SMALL_C for C_in <= 4, TC when eligible, C_in >= 64, F >= 32, else
  *            EXACT.  dwm_select_algo() reports the resolved engine. */
 typedef enum dwm_algo {
   DWM_ALGO_AUTO = 0, DWM_ALGO_EXACT = 1, DWM_ALGO_TC = 2, DWM_ALGO_SMALL_C = 3

@@ -115,7 +115,7 @@ int dwm_select_algo(const dwm_desc_t* d, int dtype, int algo) {
     case DWM_ALGO_SMALL_C: return sc_ok ? DWM_ALGO_SMALL_C : -1;
     case DWM_ALGO_AUTO:
       if (sc_ok) return DWM_ALGO_SMALL_C;
-      if (tc_ok && d->c >= 64) return DWM_ALGO_TC;
+      if (tc_ok && d->c >= 64 && d->f >= 32) return DWM_ALGO_TC;
       return DWM_ALGO_EXACT;
     default: return -1;
   }
@@ -158,8 +158,8 @@ int dwm_input_transform(const dwm_desc_t* d, int dtype, const void* x, void* V, 
 
 static int bad_algo(const dwm_desc_t* d, int algo) {
   return fail(DWM_EUNSUPPORTED,
-              "engine %d not available for this geometry/dtype (tcgen05: float32, C %% 32 == 0, "
-              "F %% 64 == 0; small-C: float32, C <= 4; got C=%d F=%d)", algo, d->c, d->f);
+              "engine %d not available for this geometry/dtype (tcgen05: float32, C %% 32 == 0; "
+              "small-C: float32, C <= 4; got C=%d F=%d)", algo, d->c, d->f);
 }
 
 int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, const void* U,

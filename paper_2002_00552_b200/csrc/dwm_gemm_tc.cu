@@ -105,7 +105,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int Q = d.num_freqs, C = d.c, F = d.f;
   const int KC = C / BK;
-  const int n_nblk = F / BN;
+  const int n_nblk = (F + BN - 1) / BN;  // a partial last block computes garbage columns, never stored
   const int64_t n_mblk = (d.tiles + BM - 1) / BM;
   const int64_t n_items = n_mblk * n_nblk;
 
@@ -362,6 +362,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
 #pragma unroll
           for (int j = 0; j < 16 && live; ++j) {
             const int f = n0 + c0 + ch + j;
+            if (f >= F) break;
             float* yf = y + ((size_t)n * F + f) * (size_t)d.oh * d.ow;
             const int oy = 2 * ty, ox = 2 * tx;
             const float v[2][2] = {{y00[j], y01[j]}, {y10[j], y11[j]}};
@@ -448,11 +449,13 @@ int make_u_map(CUtensorMap* map, const float* base, const dwm_desc_t& d) {
 }  // namespace
 
 bool tc_gemm_supported(const dwm_desc_t& d) {
-  return d.c % BK == 0 && d.f % BN == 0 && d.num_freqs <= MAX_FREQS && d.tiles < ((int64_t)1 << 31);
+  // any F: U rows past a frequency's F read the next frequency's filters (or
+  // TMA zero fill) and those accumulator columns are never stored
+  return d.c % BK == 0 && d.f >= 1 && d.num_freqs <= MAX_FREQS && d.tiles < ((int64_t)1 << 31);
 }
 
 int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag, cudaStream_t s) {
-  if (!tc_gemm_supported(d)) return fail(DWM_EUNSUPPORTED, "tcgen05 GEMM needs C %% 32 == 0 and F %% 64 == 0");
+  if (!tc_gemm_supported(d)) return fail(DWM_EUNSUPPORTED, "tcgen05 GEMM needs C %% 32 == 0");
   const float* uhi = (const float*)U;
   const float* ulo = uhi + (size_t)d.num_freqs * d.f * d.c;
   CUtensorMap mv, mh, ml;
@@ -464,7 +467,7 @@ int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, i
   int dev = 0, sms = 0;
   DWM_CUDA_TRY(cudaGetDevice(&dev));
   DWM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t items = ((d.tiles + BM - 1) / BM) * (d.f / BN);
+  const int64_t items = ((d.tiles + BM - 1) / BM) * ((d.f + BN - 1) / BN);
   const int grid = (int)(items < sms ? items : sms);
 #ifdef DWM_TC_TRACE
   static int* trace_h = nullptr;

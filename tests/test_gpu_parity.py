@@ -124,7 +124,7 @@ def test_baseline_workload_accuracy_default_engine(cuda, name):
     assert m <= MSE_TOL[engine] * gold["dwm32_mse"] * (1 + 1e-9), (engine, m, gold["dwm32_mse"])
 
 
-@pytest.mark.parametrize("case", [c for c in CASES if c["shape"][1] % 32 == 0 and c["f"] % 64 == 0],
+@pytest.mark.parametrize("case", [c for c in CASES if c["shape"][1] % 32 == 0 and c["shape"][1] >= 64],
                          ids=lambda c: c["name"])
 def test_tc_engine_on_golden_cases(cuda, case):
     d, g = ARR[f"{case['name']}/data"], ARR[f"{case['name']}/weights"]
@@ -134,6 +134,23 @@ def test_tc_engine_on_golden_cases(cuda, case):
     y64 = ARR[f"{case['name']}/direct64"]
     assert mse(y, y64) <= mse(ref32, y64)
     assert np.max(np.abs(y - ref32)) <= 4e-5 * max(1.0, np.max(np.abs(ref32)))
+
+
+@pytest.mark.parametrize("f", [40, 96, 130])
+def test_tc_engine_partial_filter_block(cuda, f):
+    """F not a multiple of the 64-filter MMA block: the last block's extra
+    columns are computed from neighbouring U rows (or TMA zero fill) and never
+    stored.  Accuracy at the reference's level, and equal per filter to a run
+    over that filter subset."""
+    rng = np.random.default_rng(f)
+    spec = ConvSpec(kernel=(5, 5), stride=(1, 1), pad=(2, 2, 2, 2))
+    d = rng.standard_normal((2, 64, 12, 12)).astype(np.float32)
+    g = rng.standard_normal((f, 64, 5, 5)).astype(np.float32)
+    y = dwm_conv2d(d, g, spec, algo="tc")
+    y64 = direct_conv2d_f64(d, g, spec)
+    assert mse(y, y64) <= mse(dwm_conv2d_oracle(d, g, spec), y64)
+    y_sub = dwm_conv2d(d, np.ascontiguousarray(g[f - 8:]), spec, algo="tc")
+    assert np.array_equal(y_sub, y[:, f - 8:])
 
 
 @pytest.mark.parametrize("name", ["cfg4-3x3s1", "cfg4-7x7s1", "cfg4-11x11s1", "cfg5-5x5s2"])
