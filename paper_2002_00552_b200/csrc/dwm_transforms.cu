@@ -211,15 +211,25 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
   });
 }
 
-template <typename T>
+template <typename T, bool WIDE>
 __global__ void __launch_bounds__(256)
-input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged) {
+input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
+                            int twb_arg, int ws_arg) {
+  // WIDE == false: whole rows staged (ws == W, one CTA per tile row) -- the
+  // common case, compiled without any of the column-block arithmetic
+  const int twb = WIDE ? twb_arg : d.tw;
+  const int ws = WIDE ? ws_arg : d.w;
   extern __shared__ __align__(16) unsigned char it_smem_raw[];
-  T* sx = reinterpret_cast<T*>(it_smem_raw);  // [IT_CB][rows_staged][W] with odd channel pitch
-  const int pitch = rows_staged * d.w + 1;
-  // channel block fastest: the C/32 CTAs of one tile row run together
-  const int ty = blockIdx.y % d.th;
-  const int n = blockIdx.y / d.th;
+  T* sx = reinterpret_cast<T*>(it_smem_raw);  // [IT_CB][rows_staged][ws] with odd channel pitch
+  const int pitch = rows_staged * ws + 1;
+  // channel block fastest: the C/32 CTAs of one tile row (segment) run together.
+  // Wide images: a CTA covers tiles [tx0, tx0 + twb) of the row and stages only
+  // the ws input columns they read (ws == W, tx0 == 0 when the row fits).
+  const int nxb = WIDE ? (d.tw + twb - 1) / twb : 1;
+  const int tx0 = WIDE ? (int)(blockIdx.y % nxb) * twb : 0;
+  const int ty = WIDE ? (int)(blockIdx.y / nxb) % d.th : (int)(blockIdx.y % d.th);
+  const int n = WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / d.th);
+  const int cbase = WIDE ? 2 * tx0 * d.s_w - d.pad_left : 0;  // input column of staged column 0
   const int c0 = blockIdx.x * IT_CB;
   const int cb = min(IT_CB, d.c - c0);
   const int row0 = 2 * ty * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
@@ -227,7 +237,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
   constexpr int VEC = 16 / sizeof(T);
   constexpr int SLOTS = 4;  // (row, vector) slots per lane: up to 128 float4 per channel row block
-  if (d.w % VEC == 0 && rows_staged * (d.w / VEC) <= 32 * SLOTS) {
+  if (!WIDE && d.w % VEC == 0 && rows_staged * (d.w / VEC) <= 32 * SLOTS) {
     // 16-byte loads; each lane owns fixed (row, vector) slots of the staged block
     const int wv = d.w / VEC, nslots = rows_staged * wv;
     const int lane = threadIdx.x % 32;
@@ -263,11 +273,11 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
       T* dst = sx + cc * pitch;
       for (int r = 0; r < rows_staged; ++r) {
         const int row = row0 + r;
-        if (row >= 0 && row < d.h) {
-          const T* src = xc + (int64_t)row * d.w;
-          for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = __ldg(src + col);
-        } else {
-          for (int col = threadIdx.x % 32; col < d.w; col += 32) dst[r * d.w + col] = T(0);
+        const bool rok = row >= 0 && row < d.h;
+        const T* src = xc + (int64_t)(rok ? row : 0) * d.w;
+        for (int sc = threadIdx.x % 32; sc < ws; sc += 32) {
+          const int col = cbase + sc;
+          dst[r * ws + sc] = (rok && col >= 0 && col < d.w) ? __ldg(src + col) : T(0);
         }
       }
     }
@@ -278,7 +288,8 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   if (lane >= cb) return;
   const T* sc = sx + lane * pitch;
   const int64_t tc_stride = d.tiles * d.c;
-  for (int tx = warp; tx < d.tw; tx += nwarps) {
+  const int tx_end = WIDE ? min(d.tw, tx0 + twb) : d.tw;
+  for (int tx = tx0 + warp; tx < tx_end; tx += nwarps) {
     const int64_t tile = ((int64_t)n * d.th + ty) * d.tw + tx;
     T* vout = V + tile * d.c + c0 + lane;
     int fq = 0;
@@ -291,7 +302,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
         const int k = 2 * ty + i;
         const int rs = R.origin + d.s_h * i;  // staged-row index
         const int row = row0 + rs;
-        rows[i] = (i < lr && k < d.oh - 1 + pr && row >= 0 && row < d.h) ? rs * d.w : -1;
+        rows[i] = (i < lr && k < d.oh - 1 + pr && row >= 0 && row < d.h) ? rs * ws : -1;
       }
       for (int cp = 0; cp < d.n_col_parts; ++cp) {
         const dwm_axis_part_t Cc = d.col_parts[cp];
@@ -301,7 +312,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
         for (int j = 0; j < 4; ++j) {
           const int k = 2 * tx + j;
           const int col = Cc.origin + d.s_w * k - d.pad_left;
-          cols[j] = (j < lc && k < d.ow - 1 + pc && col >= 0 && col < d.w) ? col : -1;
+          cols[j] = (j < lc && k < d.ow - 1 + pc && col >= 0 && col < d.w) ? col - cbase : -1;
         }
         T* vq = vout + (int64_t)fq * tc_stride;
 #define DWM_ITP(A, B) it_gather_part<A, B>(sc, rows, cols, vq, tc_stride)
@@ -338,19 +349,37 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   int rows = 0;
   for (int i = 0; i < d.n_row_parts; ++i)
     rows = max(rows, d.row_parts[i].origin + d.s_h * d.row_parts[i].count + 1);
-  const size_t smem = (size_t)IT_CB * ((size_t)rows * d.w + 1) * sizeof(T);
+  // columns the tiles [tx0, tx0 + twb) read: 2*s_w*(twb-1) + max(origin + s_w*count) + 1
+  int cols1 = 0;
+  for (int i = 0; i < d.n_col_parts; ++i)
+    cols1 = max(cols1, d.col_parts[i].origin + d.s_w * d.col_parts[i].count + 1);
   *used = false;
-  if (smem > 96 * 1024 || d.c < 8) return DWM_OK;
-  DWM_CUDA_TRY(cudaFuncSetAttribute(input_transform_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-  const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)((int64_t)d.n * d.th));
-  // warps: a divisor of the tile-row length in [4, 8] so every warp gets the same number of tiles
+  if (d.c < 8) return DWM_OK;
+  constexpr size_t CAP = 96 * 1024;
+  int twb = d.tw, ws = d.w;
+  size_t smem = (size_t)IT_CB * ((size_t)rows * ws + 1) * sizeof(T);
+  if (smem > CAP) {  // wide image: segments of the tile row, the largest multiple of 8 tiles that fits
+    twb = 0;
+    for (int t = 8; t < d.tw; t += 8) {
+      const int w_t = 2 * d.s_w * (t - 1) + cols1;
+      if ((size_t)IT_CB * ((size_t)rows * w_t + 1) * sizeof(T) <= CAP) twb = t;
+    }
+    if (twb == 0) return DWM_OK;
+    ws = 2 * d.s_w * (twb - 1) + cols1;
+    smem = (size_t)IT_CB * ((size_t)rows * ws + 1) * sizeof(T);
+  }
+  const bool wide = twb != d.tw;
+  auto kern = wide ? input_transform_smem_kernel<T, true> : input_transform_smem_kernel<T, false>;
+  DWM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int nxb = (d.tw + twb - 1) / twb;
+  const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)((int64_t)d.n * d.th * nxb));
+  // warps: a divisor of the tile count in [4, 8] so every warp gets the same number of tiles
   int warps = 8;
-  if (d.tw <= 8) warps = d.tw;
+  if (twb <= 8) warps = twb;
   else
     for (int cand = 8; cand >= 4; --cand)
-      if (d.tw % cand == 0) { warps = cand; break; }
-  input_transform_smem_kernel<T><<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows);
+      if (twb % cand == 0) { warps = cand; break; }
+  kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws);
   DWM_CUDA_TRY(cudaGetLastError());
   *used = true;
   return DWM_OK;

@@ -67,6 +67,24 @@ def test_filter_and_input_transforms_bit_exact(cuda, case, dtype):
     assert np.array_equal(v, v_ref)
 
 
+@pytest.mark.parametrize("geom", [((7, 7), (1, 1), (3, 3, 3, 3), 40, 301),    # 8 rows x 301 cols > smem cap
+                                  ((3, 3), (1, 1), (1, 1, 1, 1), 64, 230),
+                                  ((5, 5), (2, 2), (2, 1, 2, 0), 32, 419)],
+                         ids=["7x7w301", "3x3w230", "5x5s2w419"])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_input_transform_wide_rows_bit_exact(cuda, geom, dtype):
+    """Rows too wide to stage whole: the transform stages segments of the
+    tile row (column blocks); V must still be bit-identical."""
+    import torch
+    k, st, pad, c, w = geom
+    spec = ConvSpec(kernel=k, stride=st, pad=pad)
+    d = np.random.default_rng(w).standard_normal((1, c, 9, w))
+    desc = _native.make_desc(1, c, 9, w, 1, spec.kernel, spec.stride, spec.pad)
+    v_ref = input_transform_oracle(d, spec, dtype)
+    v = _stage(torch, _native.load().dwm_input_transform, desc, dtype, d.astype(dtype), v_ref.shape, cuda)
+    assert np.array_equal(v, v_ref)
+
+
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
 def test_exact_engine_matches_reference_golden(cuda, case):
     d, g = ARR[f"{case['name']}/data"], ARR[f"{case['name']}/weights"]
