@@ -14,6 +14,8 @@
 // which is the reference's rounding sequence when its BLAS accumulates
 // sequentially (small C).  Only y reaches HBM: the per-part outputs and the
 // per-frequency products stay in registers; non-finite outputs raise a flag.
+#include <cstring>
+
 #include "dwm_common.cuh"
 #include "dwm_kernels.h"
 
@@ -26,8 +28,12 @@ gemm_exact_kernel(const dwm_desc_t d, const T* __restrict__ V, const T* __restri
   constexpr int GM = BM / TM;  // threads along tiles (fast index)
   constexpr int GN = BN / TN;
   constexpr int NT = GM * GN;
-  __shared__ T sV[KC][BM + 1];
-  __shared__ T sU[KC][BN + 1];
+  constexpr int VW = 16 / sizeof(T);  // elements per 16-byte vector
+  static_assert(TM % VW == 0 || VW % TM == 0, "register tile vs vector width");
+  // thread (tm, tn) owns tiles tm*TM .. +TM-1 and filters tn*TN .. +TN-1:
+  // contiguous in smem, so the K loop reads them with 16-byte loads
+  __shared__ __align__(16) T sV[KC][BM];
+  __shared__ __align__(16) T sU[KC][BN];
 
   const int tid = threadIdx.x;
   const int tm = tid % GM, tn = tid / GM;
@@ -35,6 +41,7 @@ gemm_exact_kernel(const dwm_desc_t d, const T* __restrict__ V, const T* __restri
   const int f0 = blockIdx.y * BN;
   const int C = d.c, F = d.f;
   const int64_t tiles = d.tiles;
+  const bool vec = (C % VW) == 0;
 
   T acc[TM][TN][2][2];
   T Tt[TM][TN][2][2];
@@ -54,22 +61,69 @@ gemm_exact_kernel(const dwm_desc_t d, const T* __restrict__ V, const T* __restri
         for (int k0 = 0; k0 < C; k0 += KC) {
           const int kn = min(KC, C - k0);
           __syncthreads();
-          for (int e = tid; e < BM * KC; e += NT) {
-            const int k = e % KC, t = e / KC;
-            const int64_t tile = tile0 + t;
-            sV[k][t] = (k < kn && tile < tiles) ? Vq[tile * C + k0 + k] : T(0);
-          }
-          for (int e = tid; e < BN * KC; e += NT) {
-            const int k = e % KC, fl = e / KC;
-            sU[k][fl] = (k < kn && f0 + fl < F) ? Uq[(int64_t)(f0 + fl) * C + k0 + k] : T(0);
+          if (vec) {
+            // 16-byte loads along channels, transposed into [k][tile] / [k][filter]
+            for (int e = tid; e < BM * (KC / VW); e += NT) {
+              const int kq = e % (KC / VW), t = e / (KC / VW);
+              const int64_t tile = tile0 + t;
+              T v[VW];
+              if (tile < tiles && k0 + kq * VW < C) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(Vq + tile * C + k0 + kq * VW));
+                memcpy(v, &q, 16);
+              } else {
+#pragma unroll
+                for (int z = 0; z < VW; ++z) v[z] = T(0);
+              }
+#pragma unroll
+              for (int z = 0; z < VW; ++z) sV[kq * VW + z][t] = v[z];
+            }
+            for (int e = tid; e < BN * (KC / VW); e += NT) {
+              const int kq = e % (KC / VW), fl = e / (KC / VW);
+              T u[VW];
+              if (f0 + fl < F && k0 + kq * VW < C) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(Uq + (int64_t)(f0 + fl) * C + k0 + kq * VW));
+                memcpy(u, &q, 16);
+              } else {
+#pragma unroll
+                for (int z = 0; z < VW; ++z) u[z] = T(0);
+              }
+#pragma unroll
+              for (int z = 0; z < VW; ++z) sU[kq * VW + z][fl] = u[z];
+            }
+          } else {
+            for (int e = tid; e < BM * KC; e += NT) {
+              const int k = e % KC, t = e / KC;
+              const int64_t tile = tile0 + t;
+              sV[k][t] = (k < kn && tile < tiles) ? Vq[tile * C + k0 + k] : T(0);
+            }
+            for (int e = tid; e < BN * KC; e += NT) {
+              const int k = e % KC, fl = e / KC;
+              sU[k][fl] = (k < kn && f0 + fl < F) ? Uq[(int64_t)(f0 + fl) * C + k0 + k] : T(0);
+            }
           }
           __syncthreads();
           for (int k = 0; k < kn; ++k) {
             T vv[TM], uu[TN];
 #pragma unroll
-            for (int i = 0; i < TM; ++i) vv[i] = sV[k][tm + i * GM];
+            for (int i = 0; i < TM; i += (TM < VW ? TM : VW)) {
+              if constexpr (TM * sizeof(T) >= 16) {
+                const float4 q = *reinterpret_cast<const float4*>(&sV[k][tm * TM + i]);
+                memcpy(vv + i, &q, 16);
+              } else {
 #pragma unroll
-            for (int j = 0; j < TN; ++j) uu[j] = sU[k][tn * TN + j];
+                for (int z = 0; z < TM; ++z) vv[z] = sV[k][tm * TM + z];
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < TN; j += (TN < VW ? TN : VW)) {
+              if constexpr (TN * sizeof(T) >= 16) {
+                const float4 q = *reinterpret_cast<const float4*>(&sU[k][tn * TN + j]);
+                memcpy(uu + j, &q, 16);
+              } else {
+#pragma unroll
+                for (int z = 0; z < TN; ++z) uu[z] = sU[k][tn * TN + z];
+              }
+            }
             if (k0 + k == 0) {
 #pragma unroll
               for (int i = 0; i < TM; ++i)
@@ -132,7 +186,7 @@ gemm_exact_kernel(const dwm_desc_t d, const T* __restrict__ V, const T* __restri
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    const int64_t tile = tile0 + tm + i * GM;
+    const int64_t tile = tile0 + tm * TM + i;
     if (tile >= tiles) continue;
     const int tx = (int)(tile % d.tw);
     const int64_t t2 = tile / d.tw;
@@ -161,15 +215,17 @@ gemm_exact_kernel(const dwm_desc_t d, const T* __restrict__ V, const T* __restri
 
 int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void* U, void* y,
                       int32_t* flag, cudaStream_t s) {
-  constexpr int BM = 64, BN = 32, TM = 2, TN = 4, KC = 16;
-  const dim3 grid((unsigned)((d.tiles + BM - 1) / BM), (unsigned)((d.f + BN - 1) / BN));
-  const int threads = (BM / TM) * (BN / TN);
-  if (dtype == DWM_F64)
-    gemm_exact_kernel<double, BM, BN, TM, TN, KC><<<grid, threads, 0, s>>>(
+  if (dtype == DWM_F64) {
+    constexpr int BM = 32, BN = 64, TM = 2, TN = 4, KC = 16;
+    const dim3 grid((unsigned)((d.tiles + BM - 1) / BM), (unsigned)((d.f + BN - 1) / BN));
+    gemm_exact_kernel<double, BM, BN, TM, TN, KC><<<grid, (BM / TM) * (BN / TN), 0, s>>>(
         d, (const double*)V, (const double*)U, (double*)y, flag);
-  else
-    gemm_exact_kernel<float, BM, BN, TM, TN, KC><<<grid, threads, 0, s>>>(
+  } else {
+    constexpr int BM = 64, BN = 64, TM = 4, TN = 4, KC = 16;
+    const dim3 grid((unsigned)((d.tiles + BM - 1) / BM), (unsigned)((d.f + BN - 1) / BN));
+    gemm_exact_kernel<float, BM, BN, TM, TN, KC><<<grid, (BM / TM) * (BN / TN), 0, s>>>(
         d, (const float*)V, (const float*)U, (float*)y, flag);
+  }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }
