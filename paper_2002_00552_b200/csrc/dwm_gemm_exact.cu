@@ -376,9 +376,19 @@ int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void*
         d, (const double*)V, (const double*)U, (double*)y, flag);
   } else {
     constexpr int BM = 64, BN = 64, TM = 4, TN = 4, KC = 16;
-    const dim3 grid((unsigned)((d.tiles + BM - 1) / BM), (unsigned)((d.f + BN - 1) / BN));
-    gemm_exact_f32x2_kernel<BM, BN, TM, TN, KC><<<grid, (BM / TM) * (BN / TN), 0, s>>>(
-        d, (const float*)V, (const float*)U, (float*)y, flag);
+    const int64_t ctas = ((d.tiles + BM - 1) / BM) * ((d.f + BN - 1) / BN);
+    if (ctas < 148) {
+      // small problem (e.g. one 56x56 image): one output per thread, 16x16
+      // blocks, so the work spreads over the SMs instead of a handful of CTAs
+      constexpr int SB = 16;
+      const dim3 g2((unsigned)((d.tiles + SB - 1) / SB), (unsigned)((d.f + SB - 1) / SB));
+      gemm_exact_kernel<float, SB, SB, 1, 1, KC><<<g2, SB * SB, 0, s>>>(
+          d, (const float*)V, (const float*)U, (float*)y, flag);
+    } else {
+      const dim3 grid((unsigned)((d.tiles + BM - 1) / BM), (unsigned)((d.f + BN - 1) / BN));
+      gemm_exact_f32x2_kernel<BM, BN, TM, TN, KC><<<grid, (BM / TM) * (BN / TN), 0, s>>>(
+          d, (const float*)V, (const float*)U, (float*)y, flag);
+    }
   }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
