@@ -221,3 +221,47 @@ def test_tc_weight_grad_tail_and_determinism(cuda):
     e_tc = mse(gw1.cpu().numpy(), want)
     e_ex = mse(gw_exact.cpu().numpy(), want)
     assert e_tc <= 4 * e_ex + 1e-12, (e_tc, e_ex)
+
+
+def _random_backward_geometries(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        k = tuple(int(v) for v in rng.integers(1, 10, size=2))
+        st = tuple(int(v) for v in rng.integers(1, 4, size=2))
+        pad = tuple(int(v) for v in rng.integers(0, 4, size=4))
+        h, w = (int(v) for v in rng.integers(6, 24, size=2))
+        try:
+            ConvSpec(kernel=k, stride=st, pad=pad).out_dims(h, w)
+        except ValueError:
+            continue
+        out.append((k, st, pad, h, w))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("geom", _random_backward_geometries(24, 7),
+                         ids=lambda g: f"k{g[0]}s{g[1]}p{g[2]}_{g[3]}x{g[4]}")
+def test_backward_random_geometries(cuda, geom):
+    """Random kernels/strides/pads/extents: binary64 gradients <= 1e-10 from
+    the FP64 oracle (polyphase data gradient + CUDA-core weight gradient);
+    binary32 with the tcgen05 weight gradient close to the oracle."""
+    k, st, pad, h, w = geom
+    spec = ConvSpec(kernel=k, stride=st, pad=pad)
+    plan = plan_decomposition(spec)
+    rng = np.random.default_rng(h * 100 + w)
+    oh, ow = spec.out_dims(h, w)
+    d = rng.standard_normal((2, 3, h, w))
+    g = rng.standard_normal((5, 3, *k))
+    dy = rng.standard_normal((2, 5, oh, ow))
+    gd, gw = dwm_backward(dy, plan, d, g)
+    want_d, want_w = direct_conv2d_grads_f64(d, g, spec, dy)
+    assert np.max(np.abs(gd - want_d)) <= 1e-10
+    assert np.max(np.abs(gw - want_w)) <= 1e-10
+    d = rng.standard_normal((2, 64, h, w)).astype(np.float32)
+    g = rng.standard_normal((64, 64, *k)).astype(np.float32)
+    dy = rng.standard_normal((2, 64, oh, ow)).astype(np.float32)
+    gd, gw = dwm_backward(dy, plan, d, g, wgrad_algo="tc")
+    want_d, want_w = direct_conv2d_grads_f64(d, g, spec, dy)
+    assert np.max(np.abs(gd - want_d)) <= 2e-4 * max(1.0, np.abs(want_d).max())
+    assert np.max(np.abs(gw - want_w)) <= 2e-4 * max(1.0, np.abs(want_w).max())

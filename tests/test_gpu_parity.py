@@ -231,3 +231,55 @@ def test_full_batch_shard_invariance(cuda):
         yi = dwm_conv2d(x[i:i + 1].contiguous(), w, wl.spec())
         assert torch.equal(yi[0], y[i])
     assert torch.isfinite(y).all()
+
+
+def _random_geometries(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        r_h, r_w = (int(v) for v in rng.integers(1, 12, size=2))
+        s_h, s_w = (int(v) for v in rng.integers(1, 5, size=2))
+        pad = tuple(int(v) for v in rng.integers(0, 4, size=4))
+        h = int(rng.integers(max(1, r_h - pad[0] - pad[1]), 40))
+        w = int(rng.integers(max(1, r_w - pad[2] - pad[3]), 40))
+        try:
+            ConvSpec(kernel=(r_h, r_w), stride=(s_h, s_w), pad=pad).out_dims(h, w)
+        except ValueError:
+            continue
+        out.append(((r_h, r_w), (s_h, s_w), pad, h, w))
+    return out
+
+
+@pytest.mark.parametrize("geom", _random_geometries(64, 2024), ids=lambda g: f"k{g[0]}s{g[1]}p{g[2]}_{g[3]}x{g[4]}")
+def test_random_geometries_all_engines(cuda, geom):
+    """Randomised rectangular kernels, anisotropic strides, asymmetric pads and
+    odd extents through every engine: small-C bit-identical to the oracle;
+    exact within 4e-5 relative; tcgen05 at or below the oracle's MSE vs FP64
+    (3x slack for outputs under 4096 values, where the ratio is noise)."""
+    k, st, pad, h, w = geom
+    spec = ConvSpec(kernel=k, stride=st, pad=pad)
+    rng = np.random.default_rng(sum(k) * 100 + h * w)
+    y64_cache = {}
+    for c, f, algo in [(3, 8, "small_c"), (8, 16, "exact"), (64, 40, "tc")]:
+        d = rng.standard_normal((2, c, h, w)).astype(np.float32)
+        g = rng.standard_normal((f, c, *k)).astype(np.float32)
+        want = dwm_conv2d_oracle(d, g, spec)
+        try:
+            y = dwm_conv2d(d, g, spec, algo=algo)
+        except NotImplementedError:
+            assert algo == "small_c"  # U too large for shared memory: AUTO falls back
+            continue
+        assert y.shape == want.shape
+        if algo == "small_c":
+            tiles = 2 * -(-want.shape[2] // 2) * -(-want.shape[3] // 2)
+            if tiles >= 4:  # NumPy's GEMV order for a 1-2 tile product differs (see test_small_c_*)
+                assert np.array_equal(y, want)
+            else:
+                np.testing.assert_allclose(y, want, rtol=0, atol=1e-5 * max(1, np.abs(want).max()))
+        elif algo == "exact":
+            assert np.max(np.abs(y - want)) <= 4e-5 * max(1.0, np.abs(want).max())
+        else:
+            y64 = direct_conv2d_f64(d, g, spec)
+            # a few hundred outputs make the MSE ratio noisy: 3x slack below 4096 outputs
+            slack = 1.0 if want.size >= 4096 else 3.0
+            assert mse(y, y64) <= slack * mse(want, y64) + 1e-14
