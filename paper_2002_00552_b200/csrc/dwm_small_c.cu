@@ -90,13 +90,18 @@ __device__ __forceinline__ void consume_part(const float* __restrict__ sV, const
         const float* up = sU + (q * CC + c) * BN + tn * K::TN;
 #pragma unroll
         for (int jp = 0; jp < NP; jp += 2) {
-          if (jp + 1 < NP) {
+          // 16-byte loads need the thread's filter offset tn*TN 16-byte aligned
+          if (K::TN % 4 == 0 && jp + 1 < NP) {
             const float4 u4 = *reinterpret_cast<const float4*>(up + 2 * jp);
             u[jp] = pk(u4.x, u4.y);
             u[jp + 1] = pk(u4.z, u4.w);
           } else {
             const float2 u2 = *reinterpret_cast<const float2*>(up + 2 * jp);
             u[jp] = pk(u2.x, u2.y);
+            if (jp + 1 < NP) {
+              const float2 u3 = *reinterpret_cast<const float2*>(up + 2 * jp + 2);
+              u[jp + 1] = pk(u3.x, u3.y);
+            }
           }
         }
 #pragma unroll
@@ -353,16 +358,11 @@ template <int CC>
 int launch_cc(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
   using Wide = Cfg<CC, 2, 8>;
   using Narrow = Cfg<CC, 4, 4>;
-  if (const char* e = getenv("DWM_SC_CFG")) {  // tuning experiments only
-    if (!strcmp(e, "2x4x2")) return launch_cfg<Cfg<CC, 2, 4, 2>>(d, x, U, y, flag, s);
-    if (!strcmp(e, "2x4x1")) return launch_cfg<Cfg<CC, 2, 4, 1>>(d, x, U, y, flag, s);
-    if (!strcmp(e, "1x8x2")) return launch_cfg<Cfg<CC, 1, 8, 2>>(d, x, U, y, flag, s);
-    if (!strcmp(e, "2x8x1")) return launch_cfg<Cfg<CC, 2, 8, 1>>(d, x, U, y, flag, s);
-    if (!strcmp(e, "1x8x1")) return launch_cfg<Cfg<CC, 1, 8, 1>>(d, x, U, y, flag, s);
-    if (!strcmp(e, "1x4x2")) return launch_cfg<Cfg<CC, 1, 4, 2>>(d, x, U, y, flag, s);
-  }
   using Tall = Cfg<CC, 1, 8>;
+  using Tall6 = Cfg<CC, 1, 6>;  // 32 tiles x 48 filters: F = 96, 144, ... without a half-empty block
   if (d.f > 32 && Wide::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_cfg<Wide>(d, x, U, y, flag, s);
+  if (d.f % 64 != 0 && d.f % 48 == 0 && Tall6::smem_bytes(d.num_freqs) <= SMEM_CAP)
+    return launch_cfg<Tall6>(d, x, U, y, flag, s);
   // many frequencies (e.g. 11x11/4: 225): keep 64 filters per block -- one V
   // transform feeds twice the filters -- with a 32-tile block (cfg3: 1.34x)
   if (d.f > 32 && Tall::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_cfg<Tall>(d, x, U, y, flag, s);
