@@ -8,6 +8,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -40,12 +41,18 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         newest = max(p.stat().st_mtime for p in deps)
         if LIB.stat().st_mtime >= newest:
             return LIB
-    objs = []
-    for src in srcs:
+    extra = os.environ.get("DWM_NVCC_FLAGS", "").split()
+
+    def compile_one(src):
         obj = OUT_DIR / (src.stem + ".o")
-        extra = os.environ.get("DWM_NVCC_FLAGS", "").split()
         cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # translation units are independent: compile them concurrently
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as pool:
+        results = list(pool.map(compile_one, srcs))
+    objs = []
+    for src, obj, res in results:
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError(f"nvcc failed on {src.name}")

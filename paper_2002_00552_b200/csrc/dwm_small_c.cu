@@ -1,375 +1,12 @@
-// dwm_small_c.cu -- fully fused DWM forward for small input-channel counts
-// (C_in <= 4: the ResNet-50 / AlexNet stems of BASELINE configs[1], [2]).
-//
-// With K = C_in <= 4 the per-frequency "GEMM" is not a tensor-core
-// contraction (SURVEY §7 hard part 4); the whole forward is FP32-pipe bound
-// (FP32 FMA peak on B200 = 148 SM x 128 lanes x 1.965 GHz, measured 72 TFLOP/s
-// with tools/fp32_peak.cu).  One persistent kernel does everything on the CUDA
-// cores and only x is read and y written in HBM:
-//
-//   prologue : U[freq][F][C] (from the filter-transform kernel) -> smem,
-//              transposed to [freq][C][f-block] (resident for the whole kernel).
-//   per tile block (BM consecutive 2x2 output tiles) and per plan part:
-//     producer: polyphase gather of the part's (count+1)^2 input window for
-//               every (tile, channel) straight from x (padding and the
-//               reference's even-extension zeros by predicate), Bt.d.B row
-//               stage then column stage with compile-time coefficients ->
-//               V part in smem [q][c][tile] (double buffered; the x loads of
-//               part p+1 are issued before part p's math).
-//     consumer: per frequency, M = sum_c U*V (FMA chain, c ascending);
-//               At.m.A row stage S, column stage T with compile-time
-//               coefficients (0 skipped, +-1 as add/sub); y += T in plan
-//               order, y accumulated in shared memory.  All of it runs on
-//               packed f32x2 FFMA2/FADD2 pairs over adjacent filters, which
-//               halves FP32 issue slots (each lane of a pair is an ordinary
-//               IEEE binary32 RN operation).
-//   epilogue : interleave the 2x2 tiles into NCHW, truncate odd extents,
-//              raise the non-finite flag.
-//
-// Every rounding step is the reference's (engines.py:164-194, 244-255 with a
-// sequential BLAS), so the output equals the reference DWM in binary32 (see
-// tests/test_gpu_parity.py; only the sign of exact zeros may differ).
-#include <utility>
-
-#include "dwm_common.cuh"
-#include <cstdlib>
-#include <cstring>
-#include "dwm_kernels.h"
-#include "dwm_wino.cuh"
+// dwm_small_c.cu -- dispatch for the fused small-C forward (dwm_small_c.cuh);
+// the per-C_in kernels are instantiated in dwm_small_c_c{1..4}.cu so the
+// four heavy translation units compile in parallel.
+#include "dwm_small_c.cuh"
 
 namespace dwm {
-namespace {
-
-using namespace wino;
-
-constexpr int THREADS = 256;  // 32 tile lanes x 8 filter groups
-constexpr int MAXQ = 16;      // frequencies per part, (3+1)^2
-
-// every At row starts with +1, so no sign tracking is needed here
-template <int K, bool FIRST> __device__ __forceinline__ void chain2(f2& acc, f2 m) {
-  if constexpr (K == 0) return;
-  else if constexpr (FIRST) { static_assert(K == 1, "At rows start with +1"); acc = m; }
-  else if constexpr (K == 1) acc = add2(acc, m);
-  else acc = sub2(acc, m);
-}
-
-template <int CC_, int TM_, int TN_, int MINB_ = 1>
-struct Cfg {
-  static constexpr int CC = CC_, TM = TM_, TN = TN_, MINB = MINB_;
-  static constexpr int BM = 32 * TM;         // tiles per block
-  static constexpr int BN = 8 * TN;          // filters per block
-  static constexpr int NP = TN / 2;          // filter pairs per thread
-  static constexpr int NACC2 = TM * NP * 4;  // packed accumulators per thread
-  static constexpr int VSTAGE = MAXQ * CC * BM;
-  static size_t smem_bytes(int num_freqs) {
-    return ((size_t)NACC2 * 2 * THREADS + 2 * (size_t)VSTAGE + (size_t)num_freqs * CC * BN) * sizeof(float);
-  }
-};
-
-// Consume one part.  sV: [q][CC][BM]; sU: part's first frequency, [q][CC][BN];
-// sAcc: packed y accumulators [NACC2][THREADS] (conflict-free 8-byte slots).
-template <class K, int PR, int PC>
-__device__ __forceinline__ void consume_part(const float* __restrict__ sV, const float* __restrict__ sU,
-                                             f2* __restrict__ sAcc, int tid, bool first_part) {
-  constexpr int LR = PR + 1, LC = PC + 1, TM = K::TM, NP = K::NP, CC = K::CC, BM = K::BM, BN = K::BN;
-  const int tm = tid % 32, tn = tid / 32;
-  f2 T[TM][NP][2][2];
-  static_for<LC>([&](auto bI) {
-    constexpr int b = decltype(bI)::value;
-    f2 S[TM][NP][2];
-    static_for<LR>([&](auto aI) {
-      constexpr int a = decltype(aI)::value;
-      constexpr int q = a * LC + b;
-      f2 M[TM][NP];
-#pragma unroll
-      for (int c = 0; c < CC; ++c) {
-        float v[TM];
-#pragma unroll
-        for (int i = 0; i < TM; ++i) v[i] = sV[(q * CC + c) * BM + tm + 32 * i];
-        f2 u[NP];
-        const float* up = sU + (q * CC + c) * BN + tn * K::TN;
-#pragma unroll
-        for (int jp = 0; jp < NP; jp += 2) {
-          // 16-byte loads need the thread's filter offset tn*TN 16-byte aligned
-          if (K::TN % 4 == 0 && jp + 1 < NP) {
-            const float4 u4 = *reinterpret_cast<const float4*>(up + 2 * jp);
-            u[jp] = pk(u4.x, u4.y);
-            u[jp + 1] = pk(u4.z, u4.w);
-          } else {
-            const float2 u2 = *reinterpret_cast<const float2*>(up + 2 * jp);
-            u[jp] = pk(u2.x, u2.y);
-            if (jp + 1 < NP) {
-              const float2 u3 = *reinterpret_cast<const float2*>(up + 2 * jp + 2);
-              u[jp + 1] = pk(u3.x, u3.y);
-            }
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < TM; ++i) {
-          const f2 vv = pk(v[i], v[i]);
-#pragma unroll
-          for (int jp = 0; jp < NP; ++jp) M[i][jp] = (c == 0) ? mul2(u[jp], vv) : fma2(u[jp], vv, M[i][jp]);
-        }
-      }
-      // row stage of At.m.A: S[i'] = sum_a At_r[i'][a] M_a
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int jp = 0; jp < NP; ++jp) {
-          chain2<at_coef(PR, 0, a), (a == at_first(PR, 0))>(S[i][jp][0], M[i][jp]);
-          chain2<at_coef(PR, 1, a), (a == at_first(PR, 1))>(S[i][jp][1], M[i][jp]);
-        }
-    });
-    // column stage: T[i'][j'] = sum_b S[i'](b) * At_c[j'][b]
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int jp = 0; jp < NP; ++jp)
-#pragma unroll
-        for (int ii = 0; ii < 2; ++ii) {
-          chain2<at_coef(PC, 0, b), (b == at_first(PC, 0))>(T[i][jp][ii][0], S[i][jp][ii]);
-          chain2<at_coef(PC, 1, b), (b == at_first(PC, 1))>(T[i][jp][ii][1], S[i][jp][ii]);
-        }
-  });
-  // aggregation in plan order (tensor.py:68-81): acc = acc + T
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int jp = 0; jp < NP; ++jp)
-#pragma unroll
-      for (int ii = 0; ii < 2; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          f2* slot = sAcc + (((i * NP + jp) * 2 + ii) * 2 + jj) * THREADS + tid;
-          *slot = first_part ? T[i][jp][ii][jj] : add2(*slot, T[i][jp][ii][jj]);
-        }
-}
-
-// Producer geometry of one (tile, channel) for a tile block, computed once.
-struct ProdTile {
-  const float* xc;  // x[n][c]
-  int y0, x0;       // 2*ty*s_h - pad_top, 2*tx*s_w - pad_left
-  int ky, kx;       // 2*ty, 2*tx (window sample index base)
-  bool live;
-};
-
-__device__ __forceinline__ ProdTile prod_tile(const dwm_desc_t& d, const float* __restrict__ x, int tile, int c) {
-  ProdTile p;
-  p.live = tile < d.tiles;
-  const int t = p.live ? tile : 0;
-  const int tx = t % d.tw;
-  const int t2 = t / d.tw;
-  const int ty = t2 % d.th;
-  const int n = t2 / d.th;
-  p.xc = x + ((size_t)n * d.c + c) * (size_t)d.h * d.w;
-  p.ky = 2 * ty;
-  p.kx = 2 * tx;
-  p.y0 = 2 * ty * d.s_h - d.pad_top;
-  p.x0 = 2 * tx * d.s_w - d.pad_left;
-  return p;
-}
-
-// Producer half 1: gather the part's (count+1)^2 window into registers.
-__device__ __forceinline__ void load_window(const dwm_desc_t& d, const ProdTile& p, int rp, int cp,
-                                            float win[4][4]) {
-  const dwm_axis_part_t R = d.row_parts[rp], Cc = d.col_parts[cp];
-  int rows[4], cols[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = p.y0 + R.origin + d.s_h * i;
-    rows[i] = (p.live && i <= R.count && p.ky + i < d.oh - 1 + R.count && row >= 0 && row < d.h) ? row * d.w : -1;
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int col = p.x0 + Cc.origin + d.s_w * j;
-    cols[j] = (j <= Cc.count && p.kx + j < d.ow - 1 + Cc.count && col >= 0 && col < d.w) ? col : -1;
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? __ldg(p.xc + rows[i] + cols[j]) : 0.f;
-}
-
-// Producer half 2: Bt.d.B with compile-time coefficients -> sV[q][c][t].
-template <class K, int PR, int PC>
-__device__ __forceinline__ void transform_store(const float (&win)[4][4], float* __restrict__ sV, int t, int c) {
-  input_transform_part<PR, PC>(win, [&](int q, float v) { sV[(q * K::CC + c) * K::BM + t] = v; });
-}
-
-template <class K>
-__global__ void __launch_bounds__(THREADS, K::MINB)
-small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __restrict__ U,
-               float* __restrict__ y, int32_t* __restrict__ flag) {
-  constexpr int CC = K::CC, BM = K::BM, BN = K::BN, TM = K::TM, TN = K::TN, NP = K::NP;
-  extern __shared__ __align__(16) float smem[];
-  f2* sAcc = reinterpret_cast<f2*>(smem);                      // [NACC2][THREADS]
-  float* sVbuf = smem + K::NACC2 * 2 * THREADS;                  // [2][MAXQ][CC][BM]
-  float* sU = sVbuf + 2 * K::VSTAGE;                             // [freq][CC][BN]
-
-  const int tid = threadIdx.x;
-  const int tm = tid % 32, tn = tid / 32;
-  const int f0 = blockIdx.y * BN;
-  const int F = d.f;
-  const int nparts = d.n_row_parts * d.n_col_parts;
-  const int nblocks = (int)((d.tiles + BM - 1) / BM);
-
-  for (int e = tid; e < d.num_freqs * CC * BN; e += THREADS) {
-    const int fl = e % BN, c = (e / BN) % CC, q = e / (BN * CC);
-    const int f = f0 + fl;
-    sU[e] = f < F ? U[((size_t)q * F + f) * CC + c] : 0.f;
-  }
-
-  // producer slots: (tile t, channel c), t fastest within a warp
-  constexpr int PSLOTS = BM * CC;
-  constexpr int PPER = (PSLOTS + THREADS - 1) / THREADS;  // slots per thread (1 or 2)
-  int pt[PPER], pch[PPER];
-  bool pact[PPER];
-#pragma unroll
-  for (int s = 0; s < PPER; ++s) {
-    const int e = tid + s * THREADS;
-    pact[s] = e < PSLOTS;
-    pt[s] = e % BM;
-    pch[s] = pact[s] ? e / BM : 0;
-  }
-
-  int tb = blockIdx.x;
-  if (tb >= nblocks) return;
-  float win[PPER][4][4];
-  ProdTile ptile[PPER];
-#pragma unroll
-  for (int s = 0; s < PPER; ++s) {
-    ptile[s] = prod_tile(d, x, tb * BM + pt[s], pch[s]);
-    if (pact[s]) {
-      load_window(d, ptile[s], 0, 0, win[s]);
-#define DWM_TS0(A, B) transform_store<K, A, B>(win[s], sVbuf, pt[s], pch[s])
-      DWM_PART_SWITCH(d.row_parts[0].count, d.col_parts[0].count, DWM_TS0)
-#undef DWM_TS0
-    }
-  }
-  __syncthreads();
-
-  int stage = 0;
-  for (; tb < nblocks; tb += gridDim.x) {
-    int qoff = 0;
-    for (int p = 0; p < nparts; ++p) {
-      const int rp = p / d.n_col_parts, cpi = p % d.n_col_parts;
-      // next unit of work: part p+1 of this block, or part 0 of the next block
-      const bool last = p + 1 == nparts;
-      const bool has_next = !last || (tb + (int)gridDim.x < nblocks);
-      const int np = last ? 0 : p + 1;
-      const int nrp = np / d.n_col_parts, ncp = np % d.n_col_parts;
-#pragma unroll
-      for (int s = 0; s < PPER; ++s) {
-        if (last && has_next) ptile[s] = prod_tile(d, x, (tb + gridDim.x) * BM + pt[s], pch[s]);
-        if (pact[s] && has_next) load_window(d, ptile[s], nrp, ncp, win[s]);
-      }
-
-      const float* sV = sVbuf + stage * K::VSTAGE;
-      const float* sUp = sU + qoff * CC * BN;
-#define DWM_CONSUME(A, B) consume_part<K, A, B>(sV, sUp, sAcc, tid, p == 0)
-      DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cpi].count, DWM_CONSUME)
-#undef DWM_CONSUME
-      qoff += (d.row_parts[rp].count + 1) * (d.col_parts[cpi].count + 1);
-
-      if (has_next) {
-        float* sVn = sVbuf + (stage ^ 1) * K::VSTAGE;
-#pragma unroll
-        for (int s = 0; s < PPER; ++s) {
-          if (!pact[s]) continue;
-#define DWM_TSN(A, B) transform_store<K, A, B>(win[s], sVn, pt[s], pch[s])
-          DWM_PART_SWITCH(d.row_parts[nrp].count, d.col_parts[ncp].count, DWM_TSN)
-#undef DWM_TSN
-        }
-      }
-      stage ^= 1;
-      __syncthreads();
-    }
-    // epilogue: 2x2 tiles -> NCHW
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < TM; ++i) {
-      const int tile = tb * BM + tm + 32 * i;
-      if (tile >= d.tiles) continue;
-      const int tx = tile % d.tw;
-      const int t2 = tile / d.tw;
-      const int ty = t2 % d.th;
-      const int n = t2 / d.th;
-#pragma unroll
-      for (int jp = 0; jp < NP; ++jp) {
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const int f = f0 + tn * TN + 2 * jp + half;
-          if (f >= F) continue;
-          float* yf = y + ((size_t)n * F + f) * (size_t)d.oh * d.ow;
-#pragma unroll
-          for (int ii = 0; ii < 2; ++ii) {
-            const int oy = 2 * ty + ii;
-            if (oy >= d.oh) continue;
-            const float2 a0 = upk(sAcc[(((i * NP + jp) * 2 + ii) * 2 + 0) * THREADS + tid]);
-            const float2 a1 = upk(sAcc[(((i * NP + jp) * 2 + ii) * 2 + 1) * THREADS + tid]);
-            const float v0 = half ? a0.y : a0.x, v1 = half ? a1.y : a1.x;
-            const int ox = 2 * tx;
-            float* dst = yf + (size_t)oy * d.ow + ox;
-            if (ox + 1 < d.ow) {
-              bad |= !(isfinite(v0) && isfinite(v1));
-              if ((d.ow & 1) == 0) {
-                __stcs(reinterpret_cast<float2*>(dst), make_float2(v0, v1));
-              } else {
-                __stcs(dst, v0);
-                __stcs(dst + 1, v1);
-              }
-            } else {
-              bad |= !isfinite(v0);
-              __stcs(dst, v0);
-            }
-          }
-        }
-      }
-    }
-    if (bad && flag) *flag = 1;
-  }
-}
-
-template <class K>
-int launch_cfg(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
-  const size_t smem = K::smem_bytes(d.num_freqs);
-  DWM_CUDA_TRY(cudaFuncSetAttribute(small_c_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 0, per_sm = 0;
-  DWM_CUDA_TRY(cudaGetDevice(&dev));
-  DWM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DWM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_c_kernel<K>, THREADS, smem));
-  if (per_sm < 1) return fail(DWM_EUNSUPPORTED, "small-C kernel does not fit (smem %zu B)", smem);
-  const int fblocks = (d.f + K::BN - 1) / K::BN;
-  const int64_t nblocks = (d.tiles + K::BM - 1) / K::BM;
-  int64_t gx = ((int64_t)sms * per_sm + fblocks - 1) / fblocks;
-  if (gx > nblocks) gx = nblocks;
-  small_c_kernel<K><<<dim3((unsigned)gx, (unsigned)fblocks), THREADS, smem, s>>>(d, x, U, y, flag);
-  DWM_CUDA_TRY(cudaGetLastError());
-  return DWM_OK;
-}
-
-constexpr size_t SMEM_CAP = 220 * 1024;
-
-// Wide variant (2 tiles x 8 filters per thread, 64x64 block) when its resident
-// U fits; else Tall (1 x 8, 32x64 block); else Narrow (4 x 4, 128x32 block).
-// (Measured on cfg2/cfg3 against 2x4, 1x4, 1x8 with 2 CTAs/SM: see DESIGN.md.)
-template <int CC>
-int launch_cc(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
-  using Wide = Cfg<CC, 2, 8>;
-  using Narrow = Cfg<CC, 4, 4>;
-  using Tall = Cfg<CC, 1, 8>;
-  using Tall6 = Cfg<CC, 1, 6>;  // 32 tiles x 48 filters: F = 96, 144, ... without a half-empty block
-  if (d.f > 32 && Wide::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_cfg<Wide>(d, x, U, y, flag, s);
-  if (d.f % 64 != 0 && d.f % 48 == 0 && Tall6::smem_bytes(d.num_freqs) <= SMEM_CAP)
-    return launch_cfg<Tall6>(d, x, U, y, flag, s);
-  // many frequencies (e.g. 11x11/4: 225): keep 64 filters per block -- one V
-  // transform feeds twice the filters -- with a 32-tile block (cfg3: 1.34x)
-  if (d.f > 32 && Tall::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_cfg<Tall>(d, x, U, y, flag, s);
-  return launch_cfg<Narrow>(d, x, U, y, flag, s);
-}
-
-}  // namespace
+using smallc::Cfg;
+using smallc::SMEM_CAP;
+using smallc::launch_cc;
 
 bool small_c_supported(const dwm_desc_t& d) {
   if (d.c < 1 || d.c > 4) return false;

@@ -1,0 +1,8 @@
+// dwm_small_c_c2.cu -- small-C forward kernels for C_in = 2 (see dwm_small_c.cuh)
+#include "dwm_small_c.cuh"
+
+namespace dwm {
+namespace smallc {
+template int launch_cc<2>(const dwm_desc_t&, const float*, const float*, float*, int32_t*, cudaStream_t);
+}  // namespace smallc
+}  // namespace dwm
