@@ -97,6 +97,19 @@ def _check_pair(data, weights):
 _WORKSPACE = {}
 
 
+def _zeros_like_io(ref, shape, dt, out=None):
+    """Zeros of ``shape`` in the caller's container type (NumPy, or torch on
+    the reference tensor's device) -- the result of an empty contraction."""
+    if out is not None:
+        out.zero_()
+        return out
+    if _is_torch(ref):
+        torch = _torch()
+        tdt = torch.float64 if np.dtype(dt) == np.dtype(np.float64) else torch.float32
+        return torch.zeros(shape, dtype=tdt, device=ref.device)
+    return np.zeros(shape, dtype=dt)
+
+
 def _workspace(device, nbytes: int, stream=None):
     """Grow-only per-device scratch for V and U (stream-ordered reuse).  When
     the kernels using it run on a stream other than the allocating (current)
@@ -144,7 +157,13 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
     dt = _np_dtype(data) if precision is None else precision_dtype(precision)
     n, c, h, w = (int(s) for s in data.shape)
     f = int(weights.shape[0])
-    spec.out_dims(h, w)  # geometry errors with the reference's message
+    oh, ow = spec.out_dims(h, w)  # geometry errors with the reference's message
+    if n == 0 or c == 0 or f == 0:
+        # empty batch / filters -> empty output; no input channels -> zeros (the
+        # empty sum), exactly as the reference's NumPy path returns
+        if counter is not None:
+            counter.elementwise += flops_dwm(plan, (oh, ow))
+        return _zeros_like_io(data, (n, f, oh, ow), dt, out)
 
     torch = _torch()
     lib = _native.load()
@@ -345,6 +364,11 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
     if tuple(grad_out.shape) != (n, f, oh, ow):
         raise ValueError(f"grad_out shape {tuple(grad_out.shape)} != {(n, f, oh, ow)}")
     dt = _np_dtype(grad_out) if precision is None else precision_dtype(precision)
+    if n == 0 or c == 0 or f == 0:
+        # empty contraction: both gradients are zeros (the reference's result)
+        gd = _zeros_like_io(grad_out, (n, c, h, w), dt) if need_data else None
+        gw = _zeros_like_io(grad_out, (f, c, *spec.kernel), dt) if need_weights else None
+        return gd, gw
 
     torch = _torch()
     lib = _native.load()

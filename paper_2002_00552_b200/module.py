@@ -80,6 +80,9 @@ def _forward(x: torch.Tensor, w: torch.Tensor, spec: ConvSpec, algo: str, cache:
         raise ValueError(f"channel mismatch: data has {x.shape[1]}, weights have {w.shape[1]}")
     if tuple(w.shape[2:]) != spec.kernel:
         raise ValueError(f"weights taps {tuple(w.shape[2:])} do not match kernel {spec.kernel}")
+    if x.shape[0] == 0 or x.shape[1] == 0 or w.shape[0] == 0:
+        oh, ow = spec.out_dims(int(x.shape[2]), int(x.shape[3]))
+        return torch.zeros((x.shape[0], w.shape[0], oh, ow), dtype=x.dtype, device=x.device)
     lib = _native.load()
     code = _native.DWM_F64 if x.dtype == torch.float64 else _native.DWM_F32
     algo_code = _native.ALGOS[algo]

@@ -44,3 +44,32 @@ def test_no_cpu_fallback_without_gpu():
         dwm_conv2d(np.zeros((1, 1, 8, 8)), np.zeros((1, 1, 3, 3)), ConvSpec(kernel=(3, 3)))
     with pytest.raises(ValueError, match="only 'dwm'"):
         convolve(np.zeros((1, 1, 8, 8)), np.zeros((1, 1, 3, 3)), ConvSpec(kernel=(3, 3)), algo="direct")
+
+
+@pytest.mark.parametrize("n,c,f", [(0, 3, 4), (2, 3, 0), (2, 0, 4), (0, 0, 0)])
+def test_empty_tensors_like_reference(n, c, f):
+    """Empty batch / filters give empty outputs and no input channels gives
+    zeros, as the reference's NumPy path does; the counter still counts.
+    (Shape-only: no device work happens, so this runs on CPU.)"""
+    import numpy as np
+    from paper_2002_00552_b200 import ConvSpec, FlopCounter, dwm_backward, dwm_conv2d, flops_dwm, plan_decomposition
+    spec = ConvSpec(kernel=(3, 3), stride=(2, 1), pad=(1, 0, 1, 1))
+    d = np.zeros((n, c, 8, 9), np.float32)
+    g = np.ones((f, c, 3, 3), np.float32)
+    counter = FlopCounter()
+    y = dwm_conv2d(d, g, spec, counter=counter)
+    oh, ow = spec.out_dims(8, 9)
+    assert y.shape == (n, f, oh, ow) and y.dtype == np.float32 and not y.any()
+    assert counter.elementwise == flops_dwm(plan_decomposition(spec), (oh, ow))
+    gd, gw = dwm_backward(np.ones((n, f, oh, ow), np.float32), plan_decomposition(spec), d, g)
+    assert gd.shape == d.shape and gw.shape == g.shape and not gd.any() and not gw.any()
+
+
+def test_empty_tensors_match_live_reference(ref):
+    import numpy as np
+    from paper_2002_00552_b200 import ConvSpec, dwm_conv2d
+    d = np.zeros((2, 0, 8, 8), np.float32)
+    g = np.ones((4, 0, 3, 3), np.float32)
+    want = ref.dwm_conv2d(d, g, ref.ConvSpec(kernel=(3, 3)))
+    got = dwm_conv2d(d, g, ConvSpec(kernel=(3, 3)))
+    assert got.shape == want.shape and got.dtype == want.dtype and np.array_equal(got, want)
