@@ -127,6 +127,24 @@ def _workspace(device, nbytes: int, stream=None):
     return buf
 
 
+def _batch_chunk(lib, desc, code, algo_code, spec, dev, budget=None) -> int:
+    """Largest batch chunk whose workspace fits the device memory budget
+    (free memory plus the cached workspace, with 20 % headroom); the whole
+    batch when it fits."""
+    n = desc.n
+    need = lib.dwm_workspace_bytes(desc, code, algo_code)
+    if budget is None:
+        torch = _torch()
+        free, _ = torch.cuda.mem_get_info(dev)
+        cached = _WORKSPACE.get(dev)
+        budget = int(0.8 * (free + (cached.numel() if cached is not None else 0)))
+    if need <= budget or n <= 1:
+        return max(n, 1)
+    one = lib.dwm_workspace_bytes(_native.make_desc(1, desc.c, desc.h, desc.w, desc.f, spec.kernel,
+                                                    spec.stride, spec.pad), code, algo_code)
+    return int(max(1, min(n, budget // max(one, 1))))
+
+
 def _check_plan_matches(plan: DecompositionPlan, desc) -> None:
     rows = [(p.origin, p.step, p.count) for p in plan.row_parts]
     cols = [(p.origin, p.step, p.count) for p in plan.col_parts]
@@ -203,13 +221,20 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
         else:
             x_d = data.to(dev, dtype=tdt).contiguous()
             y_d = out if out is not None else torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
-            ws_bytes = lib.dwm_workspace_bytes(desc, code, algo_code)
-            ws = _workspace(dev, ws_bytes, s)
-            st = lib.dwm_conv2d_forward(desc, code, algo_code, x_d.data_ptr(), w_d.data_ptr(),
-                                        y_d.data_ptr(), ws.data_ptr(), ws_bytes,
-                                        flag.data_ptr() if flag is not None else None,
-                                        s.cuda_stream)
-            _native.check(st, "dwm_conv2d_forward")
+            # images are independent: when the V workspace of the whole batch
+            # would not fit, run it in batch chunks (same bits per image)
+            chunk = _batch_chunk(lib, desc, code, algo_code, spec, dev)
+            for b0 in range(0, n, chunk):
+                b1 = min(n, b0 + chunk)
+                dk = desc if (b0, b1) == (0, n) else _native.make_desc(
+                    b1 - b0, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+                ws_bytes = lib.dwm_workspace_bytes(dk, code, algo_code)
+                ws = _workspace(dev, ws_bytes, s)
+                st = lib.dwm_conv2d_forward(dk, code, algo_code, x_d[b0].data_ptr(), w_d.data_ptr(),
+                                            y_d[b0].data_ptr(), ws.data_ptr(), ws_bytes,
+                                            flag.data_ptr() if flag is not None else None,
+                                            s.cuda_stream)
+                _native.check(st, "dwm_conv2d_forward")
             y_res = y_d
         if counter is not None:
             counter.elementwise += int(lib.dwm_elementwise_count(desc))

@@ -283,3 +283,25 @@ def test_random_geometries_all_engines(cuda, geom):
             # a few hundred outputs make the MSE ratio noisy: 3x slack below 4096 outputs
             slack = 1.0 if want.size >= 4096 else 3.0
             assert mse(y, y64) <= slack * mse(want, y64) + 1e-14
+
+
+def test_batch_chunking_when_workspace_exceeds_budget(cuda, monkeypatch):
+    """A batch whose V workspace exceeds the memory budget runs in chunks;
+    every image is bit-identical to the unchunked run."""
+    import torch
+    from paper_2002_00552_b200 import engines
+    spec = ConvSpec(kernel=(5, 5), stride=(1, 1), pad=(2, 2, 2, 2))
+    x = torch.randn(5, 64, 12, 12, device=cuda)
+    w = torch.randn(64, 64, 5, 5, device=cuda)
+    y_full = dwm_conv2d(x, w, spec)
+    calls = []
+    real = engines._batch_chunk
+
+    def small_budget(lib, desc, code, algo_code, spec_, dev, budget=None):
+        k = real(lib, desc, code, algo_code, spec_, dev, budget=1)
+        calls.append(k)
+        return k
+    monkeypatch.setattr(engines, "_batch_chunk", small_budget)
+    y_chunked = dwm_conv2d(x, w, spec)
+    assert calls == [1]
+    assert torch.equal(y_full, y_chunked)
