@@ -211,8 +211,11 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
   });
 }
 
+#ifndef DWM_IT_MINB
+#define DWM_IT_MINB 4  // 56 registers: 5 CTAs of 224 threads per SM (tools/it_exp.sh)
+#endif
 template <typename T, bool WIDE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, DWM_IT_MINB)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
                             int twb_arg, int ws_arg) {
   // WIDE == false: whole rows staged (ws == W, one CTA per tile row) -- the
