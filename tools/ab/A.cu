@@ -197,17 +197,14 @@ constexpr int IT_CB = 32;  // channels per CTA (one per lane)
 
 // Window gather (compile-time extent, predicated zeros) + Bt.d.B + stores
 // to consecutive frequency planes through a running pointer.
-template <int PR, int PC, bool CHECK, typename T>
+template <int PR, int PC, typename T>
 __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const int (&rows)[4], const int (&cols)[4],
                                                T* vq, int64_t stride) {
-  // the staged block is zero-padded, so only the even-extension truncation
-  // at an odd last tile row / column needs a predicate (CHECK)
   T win[4][4];
 #pragma unroll
   for (int i = 0; i <= PR; ++i)
 #pragma unroll
-    for (int j = 0; j <= PC; ++j)
-      win[i][j] = (!CHECK || (rows[i] >= 0 && cols[j] >= 0)) ? sc[rows[i] + cols[j]] : T(0);
+    for (int j = 0; j <= PC; ++j) win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? sc[rows[i] + cols[j]] : T(0);
   wino::input_transform_part<PR, PC>(win, [&](int, T v) {
     *vq = v;
     vq += stride;
@@ -224,7 +221,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   // WIDE == false: whole rows staged (ws == W, one CTA per tile row) -- the
   // common case, compiled without any of the column-block arithmetic
   const int twb = WIDE ? twb_arg : d.tw;
-  const int ws = WIDE ? ws_arg : d.pad_left + d.w + d.pad_right;  // staged row width (zero-padded)
+  const int ws = WIDE ? ws_arg : d.w;
   extern __shared__ __align__(16) unsigned char it_smem_raw[];
   T* sx = reinterpret_cast<T*>(it_smem_raw);  // [IT_CB][rows_staged][ws] with odd channel pitch
   const int pitch = rows_staged * ws + 1;
@@ -235,7 +232,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   const int tx0 = WIDE ? (int)(blockIdx.y % nxb) * twb : 0;
   const int ty = WIDE ? (int)(blockIdx.y / nxb) % d.th : (int)(blockIdx.y % d.th);
   const int n = WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / d.th);
-  const int cbase = WIDE ? 2 * tx0 * d.s_w - d.pad_left : -d.pad_left;  // input column of staged column 0
+  const int cbase = WIDE ? 2 * tx0 * d.s_w - d.pad_left : 0;  // input column of staged column 0
   const int c0 = blockIdx.x * IT_CB;
   const int cb = min(IT_CB, d.c - c0);
   const int row0 = 2 * ty * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
@@ -257,11 +254,6 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
     for (int cc = threadIdx.x / 32; cc < cb; cc += blockDim.x / 32) {
       const T* xc = x + ((int64_t)n * d.c + c0 + cc) * d.h * d.w;
       T* dst = sx + cc * pitch;
-      // zero pad columns (left and right of every staged row)
-      if (lane < d.pad_left + d.pad_right) {
-        const int zc = lane < d.pad_left ? lane : d.w + lane;
-        for (int r = 0; r < rows_staged; ++r) dst[r * ws + zc] = T(0);
-      }
 #pragma unroll
       for (int k = 0; k < SLOTS; ++k) {
         if (srow[k] < 0) continue;
@@ -275,7 +267,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
           for (int e = 0; e < VEC; ++e) v[e] = T(0);
         }
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) dst[srow[k] * ws + d.pad_left + scol[k] + e] = v[e];
+        for (int e = 0; e < VEC; ++e) dst[srow[k] * d.w + scol[k] + e] = v[e];
       }
     }
   } else {
@@ -304,8 +296,6 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
     const int64_t tile = ((int64_t)n * d.th + ty) * d.tw + tx;
     T* vout = V + tile * d.c + c0 + lane;
     int fq = 0;
-    // even-extension truncation only reaches an odd last tile row / column
-    const bool check = 2 * ty >= d.oh - 1 || 2 * tx >= d.ow - 1;
     for (int rp = 0; rp < d.n_row_parts; ++rp) {
       const dwm_axis_part_t R = d.row_parts[rp];
       const int pr = R.count, lr = pr + 1;
@@ -313,8 +303,9 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = 2 * ty + i;
-        const int rs = R.origin + d.s_h * i;  // staged-row index (rows outside x are staged zeros)
-        rows[i] = (i < lr && k < d.oh - 1 + pr) ? rs * ws : -1;
+        const int rs = R.origin + d.s_h * i;  // staged-row index
+        const int row = row0 + rs;
+        rows[i] = (i < lr && k < d.oh - 1 + pr && row >= 0 && row < d.h) ? rs * ws : -1;
       }
       for (int cp = 0; cp < d.n_col_parts; ++cp) {
         const dwm_axis_part_t Cc = d.col_parts[cp];
@@ -323,19 +314,13 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int k = 2 * tx + j;
-          const int col = Cc.origin + d.s_w * k - d.pad_left;  // staged columns cover every col read
-          cols[j] = (j < lc && k < d.ow - 1 + pc) ? col - cbase : -1;
+          const int col = Cc.origin + d.s_w * k - d.pad_left;
+          cols[j] = (j < lc && k < d.ow - 1 + pc && col >= 0 && col < d.w) ? col - cbase : -1;
         }
         T* vq = vout + (int64_t)fq * tc_stride;
-        if (check) {
-#define DWM_ITP(A, B) it_gather_part<A, B, true>(sc, rows, cols, vq, tc_stride)
-          DWM_PART_SWITCH(pr, pc, DWM_ITP)
+#define DWM_ITP(A, B) it_gather_part<A, B>(sc, rows, cols, vq, tc_stride)
+        DWM_PART_SWITCH(pr, pc, DWM_ITP)
 #undef DWM_ITP
-        } else {
-#define DWM_ITP(A, B) it_gather_part<A, B, false>(sc, rows, cols, vq, tc_stride)
-          DWM_PART_SWITCH(pr, pc, DWM_ITP)
-#undef DWM_ITP
-        }
         fq += lr * lc;
       }
     }
@@ -374,7 +359,7 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   *used = false;
   if (d.c < 8) return DWM_OK;
   constexpr size_t CAP = 96 * 1024;
-  int twb = d.tw, ws = d.pad_left + d.w + d.pad_right;  // whole zero-padded rows
+  int twb = d.tw, ws = d.w;
   size_t smem = (size_t)IT_CB * ((size_t)rows * ws + 1) * sizeof(T);
   if (smem > CAP) {  // wide image: segments of the tile row, the largest multiple of 8 tiles that fits
     twb = 0;
