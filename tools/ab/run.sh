@@ -1,3 +1,4 @@
+# usage: put the two versions at tools/ab/A.cu and tools/ab/B.cu (git-ignored), then run on the GPU box
 # A/B timing of two versions of one source file on the same box (dev tool)
 F=paper_2002_00552_b200/csrc/dwm_transforms.cu
 for v in ${VARIANTS:-A B A B}; do
