@@ -257,11 +257,9 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             tc_fence_after();
             const uint32_t base = lane_addr + COL_A + sa * (2 * AK);
 #ifndef DWM_EXP_NO_CONV_ST
-#pragma unroll
-            for (int c = 0; c < AK; c += 16) {
-              tmem_st16(base + c, *reinterpret_cast<float(*)[16]>(hi + h * AK + c));
-              tmem_st16(base + AK + c, *reinterpret_cast<float(*)[16]>(lo + h * AK + c));
-            }
+            static_assert(AK == 32, "one x32 TMEM store per operand half");
+            tmem_st32(base, *reinterpret_cast<float(*)[32]>(hi + h * AK));
+            tmem_st32(base + AK, *reinterpret_cast<float(*)[32]>(lo + h * AK));
 #else
             if (hi[0] == 12345.f) tmem_st16(base, *reinterpret_cast<float(*)[16]>(hi));
 #endif
@@ -337,7 +335,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             for (int j = 0; j < EC; ++j) yv[j] = __fsub_rn(yv[j], mq[j]);
           }
 #pragma unroll
-          for (int ch = 0; ch < EC; ch += 16) tmem_st16(ya + ch, *reinterpret_cast<float(*)[16]>(yv + ch));
+          tmem_st32(ya, yv);
         }
         tmem_st_wait();
       }
