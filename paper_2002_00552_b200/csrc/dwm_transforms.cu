@@ -214,11 +214,11 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
   });
 }
 
-#ifndef DWM_IT_MINB
-#define DWM_IT_MINB 4  // 56 registers: 5 CTAs of 224 threads per SM (tools/it_exp.sh)
+#ifndef DWM_IT_MAXNREG
+#define DWM_IT_MAXNREG 56  // 5 CTAs of 224 threads per SM (tools/it_exp.sh); binary64 spills a little
 #endif
 template <typename T, bool WIDE>
-__global__ void __launch_bounds__(256, DWM_IT_MINB)
+__global__ void __maxnreg__(DWM_IT_MAXNREG)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
                             int twb_arg, int ws_arg) {
   // WIDE == false: whole rows staged (ws == W, one CTA per tile row) -- the
@@ -242,40 +242,38 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
   constexpr int VEC = 16 / sizeof(T);
-  constexpr int SLOTS = 4;  // (row, vector) slots per lane: up to 128 float4 per channel row block
-  if (!WIDE && d.w % VEC == 0 && rows_staged * (d.w / VEC) <= 32 * SLOTS) {
-    // 16-byte loads; each lane owns fixed (row, vector) slots of the staged block
-    const int wv = d.w / VEC, nslots = rows_staged * wv;
-    const int lane = threadIdx.x % 32;
-    int srow[SLOTS], scol[SLOTS];
-#pragma unroll
-    for (int k = 0; k < SLOTS; ++k) {
-      const int p = lane + 32 * k;
-      srow[k] = p < nslots ? p / wv : -1;
-      scol[k] = p < nslots ? (p % wv) * VEC : 0;
+  if (!WIDE && d.w % VEC == 0) {
+    // 16-byte loads over the flattened (channel, row, vector) space, four per
+    // thread in flight before the first smem store waits on one
+    const int wv = d.w / VEC, nslots = rows_staged * wv, nitems = cb * nslots;
+    const int npad = d.pad_left + d.pad_right;
+    for (int p = threadIdx.x; p < cb * rows_staged * npad; p += blockDim.x) {
+      const int cc = p / (rows_staged * npad), rz = p - cc * rows_staged * npad;
+      const int r = rz / npad, z = rz - r * npad;
+      sx[cc * pitch + r * ws + (z < d.pad_left ? z : d.w + z)] = T(0);
     }
-    for (int cc = threadIdx.x / 32; cc < cb; cc += blockDim.x / 32) {
-      const T* xc = x + ((int64_t)n * d.c + c0 + cc) * d.h * d.w;
-      T* dst = sx + cc * pitch;
-      // zero pad columns (left and right of every staged row)
-      if (lane < d.pad_left + d.pad_right) {
-        const int zc = lane < d.pad_left ? lane : d.w + lane;
-        for (int r = 0; r < rows_staged; ++r) dst[r * ws + zc] = T(0);
+    constexpr int U = 4;
+    for (int p0 = threadIdx.x; p0 < nitems; p0 += U * blockDim.x) {
+      float4 q[U];
+      int dsto[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = p0 + u * blockDim.x;
+        const int cc = p / nslots, rs = p - cc * nslots;
+        const int sr = rs / wv, scv = (rs - sr * wv) * VEC;
+        const int row = row0 + sr;
+        const bool ok = p < nitems && row >= 0 && row < d.h;
+        q[u] = ok ? __ldg(reinterpret_cast<const float4*>(x + (((int64_t)n * d.c + c0 + cc) * d.h + row) * d.w + scv))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        dsto[u] = p < nitems ? cc * pitch + sr * ws + d.pad_left + scv : -1;
       }
 #pragma unroll
-      for (int k = 0; k < SLOTS; ++k) {
-        if (srow[k] < 0) continue;
-        const int row = row0 + srow[k];
+      for (int u = 0; u < U; ++u) {
+        if (dsto[u] < 0) break;
         T v[VEC];
-        if (row >= 0 && row < d.h) {
-          const float4 q = __ldg(reinterpret_cast<const float4*>(xc + (int64_t)row * d.w + scol[k]));
-          memcpy(v, &q, 16);
-        } else {
+        memcpy(v, &q[u], 16);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) v[e] = T(0);
-        }
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) dst[srow[k] * ws + d.pad_left + scol[k] + e] = v[e];
+        for (int e = 0; e < VEC; ++e) sx[dsto[u] + e] = v[e];
       }
     }
   } else {

@@ -12,4 +12,4 @@ import json,sys,os; d=json.loads(sys.stdin.read()); k={x['name']:x for x in d['k
   done
   echo $line
 done
-cp tools/ab/B.cu $F
+cp tools/ab/${FINAL:-B}.cu $F

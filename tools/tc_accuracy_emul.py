@@ -7,8 +7,11 @@ the tensor core; U: hi/lo both RNA), the 8 products of one K=8 MMA step are
 summed exactly, and the FP32 accumulator update truncates toward zero.
 
 Schemes:
-  chunk32   fresh accumulator per 32 channels: 8 correction steps, then 4
-            main steps; chunks summed in FP32 RN (the shipped kernel)
+  chunk<S>  fresh accumulator per S channels (S a multiple of 32); per 32
+            channels 8 correction steps, then 4 main steps; chunks summed in
+            FP32 RN (chunk32: the shipped kernel for C = 64)
+  cfirst<S> fresh accumulator per S channels: all 2S/8 correction steps,
+            then the S/8 main steps
   split<K>  main (hi*hi) accumulator per K channels, one correction
             accumulator over all channels; mq = sum(main chunks) + corr
   long      one accumulator over all channels (corr first per 32 ch)
@@ -59,20 +62,34 @@ def contraction(V, U, scheme):
     uh = rna_tf32(U)
     ul = rna_tf32((U - uh).astype(np.float32))
     ks = [slice(8 * k, 8 * k + 8) for k in range(C // 8)]
-    if scheme == "chunk32" or scheme == "long":
+    if scheme.startswith("chunk") or scheme == "long":
+        span = int(scheme[len("chunk"):]) if scheme != "long" else C
         mq = None
         acc = None
         for c0 in range(0, C, 32):
             kk = ks[c0 // 8:c0 // 8 + 4]
-            fresh = scheme == "chunk32" or c0 == 0
+            fresh = c0 % span == 0
             for i, k in enumerate(kk):
                 acc = step(acc, vh[..., k], ul[..., k], fresh and i == 0)
                 acc = step(acc, vl[..., k], uh[..., k], False)
             for k in kk:
                 acc = step(acc, vh[..., k], uh[..., k], False)
-            if scheme == "chunk32":
+            if scheme != "long" and (c0 + 32) % span == 0:
                 mq = acc if mq is None else (mq + acc).astype(np.float32)
         return acc if scheme == "long" else mq
+    if scheme.startswith("cfirst"):
+        span = int(scheme[len("cfirst"):])
+        mq = None
+        for c0 in range(0, C, span):
+            kk = ks[c0 // 8:(c0 + span) // 8]
+            acc = None
+            for i, k in enumerate(kk):
+                acc = step(acc, vh[..., k], ul[..., k], i == 0)
+                acc = step(acc, vl[..., k], uh[..., k], False)
+            for k in kk:
+                acc = step(acc, vh[..., k], uh[..., k], False)
+            mq = acc if mq is None else (mq + acc).astype(np.float32)
+        return mq
     kch = int(scheme[len("split"):])
     corr = None
     mq = None
