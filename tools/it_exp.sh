@@ -1,4 +1,4 @@
-for m in 1 4 5; do
+for m in 48 56 64; do
   DWM_NVCC_FLAGS="-DDWM_IT_MAXNREG=$m" python -m paper_2002_00552_b200.build > /dev/null 2>&1
   echo "MAXNREG=$m"
   for w in cfg4-3x3s1 cfg4-7x7s1 cfg4-11x11s1 cfg5-3x3s2 cfg5-5x5s2; do
