@@ -252,7 +252,10 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
       const int r = rz / npad, z = rz - r * npad;
       sx[cc * pitch + r * ws + (z < d.pad_left ? z : d.w + z)] = T(0);
     }
-    constexpr int U = 4;
+#ifndef DWM_IT_LOADS
+#define DWM_IT_LOADS 4
+#endif
+    constexpr int U = DWM_IT_LOADS;
     for (int p0 = threadIdx.x; p0 < nitems; p0 += U * blockDim.x) {
       float4 q[U];
       int dsto[U];
