@@ -194,10 +194,22 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
 // segment of V[fq][tile][c].  Same arithmetic (and bits) as the kernel above.
 // ---------------------------------------------------------------------------
 constexpr int IT_CB = 32;  // channels per CTA (one per lane)
+#ifndef DWM_IT_TROWS
+#define DWM_IT_TROWS 4  // tile rows per CTA (whole-row staging, few-frequency plans)
+#endif
+// Measured: 4 tile rows per CTA take cfg4 3x3 from
+// 0.452 to 0.411 ms; every plan with more frequencies got slower with 2 or 4
+// (7x7: +14 %, cfg5 3x3/2: +3 %), so only single-part F(2,<=3) plans use it.
+constexpr int IT_TROWS_MAX_FREQS = 16;
+constexpr int IT_STREAM_MIN_FREQS = 64;  // evict-first V stores above this many frequencies
 
 // Window gather (compile-time extent, predicated zeros) + Bt.d.B + stores
-// to consecutive frequency planes through a running pointer.
-template <int PR, int PC, bool CHECK, typename T>
+// to consecutive frequency planes through a running pointer.  STREAM: V
+// stores with the evict-first hint (st.global.cs) -- measured faster for the
+// many-frequency plans (V/x >= 25: cfg4 7x7 -9 %, 11x11 -7 %), slower for
+// 3x3 (+4 %: there the staged-row overlap between neighbouring tile rows is
+// re-read from L2), see DESIGN.md section 3.3.
+template <int PR, int PC, bool CHECK, bool STREAM, typename T>
 __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const int (&rows)[4], const int (&cols)[4],
                                                T* vq, int64_t stride) {
   // the staged block is zero-padded, so only the even-extension truncation
@@ -209,7 +221,8 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
     for (int j = 0; j <= PC; ++j)
       win[i][j] = (!CHECK || (rows[i] >= 0 && cols[j] >= 0)) ? sc[rows[i] + cols[j]] : T(0);
   wino::input_transform_part<PR, PC>(win, [&](int, T v) {
-    *vq = v;
+    if constexpr (STREAM) __stcs(vq, v);
+    else *vq = v;
     vq += stride;
   });
 }
@@ -217,13 +230,14 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
 #ifndef DWM_IT_MAXNREG
 #define DWM_IT_MAXNREG 56  // 5 CTAs of 224 threads per SM (tools/it_exp.sh); binary64 spills a little
 #endif
-template <typename T, bool WIDE>
+template <typename T, bool WIDE, bool STREAM>
 __global__ void __maxnreg__(DWM_IT_MAXNREG)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
-                            int twb_arg, int ws_arg) {
-  // WIDE == false: whole rows staged (ws == W, one CTA per tile row) -- the
+                            int twb_arg, int ws_arg, int trows_arg) {
+  // WIDE == false: whole rows staged (ws == W, trows tile rows per CTA) -- the
   // common case, compiled without any of the column-block arithmetic
   const int twb = WIDE ? twb_arg : d.tw;
+  const int trows = WIDE ? 1 : trows_arg;  // tile rows per CTA (their staged rows overlap)
   const int ws = WIDE ? ws_arg : d.pad_left + d.w + d.pad_right;  // staged row width (zero-padded)
   extern __shared__ __align__(16) unsigned char it_smem_raw[];
   T* sx = reinterpret_cast<T*>(it_smem_raw);  // [IT_CB][rows_staged][ws] with odd channel pitch
@@ -233,12 +247,13 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   // the ws input columns they read (ws == W, tx0 == 0 when the row fits).
   const int nxb = WIDE ? (d.tw + twb - 1) / twb : 1;
   const int tx0 = WIDE ? (int)(blockIdx.y % nxb) * twb : 0;
-  const int ty = WIDE ? (int)(blockIdx.y / nxb) % d.th : (int)(blockIdx.y % d.th);
-  const int n = WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / d.th);
+  const int nty = WIDE ? d.th : (d.th + trows - 1) / trows;
+  const int ty0 = WIDE ? (int)(blockIdx.y / nxb) % d.th : (int)(blockIdx.y % nty) * trows;
+  const int n = WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / nty);
   const int cbase = WIDE ? 2 * tx0 * d.s_w - d.pad_left : -d.pad_left;  // input column of staged column 0
   const int c0 = blockIdx.x * IT_CB;
   const int cb = min(IT_CB, d.c - c0);
-  const int row0 = 2 * ty * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
+  const int row0 = 2 * ty0 * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
 
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
   constexpr int VEC = 16 / sizeof(T);
@@ -301,7 +316,10 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   const T* sc = sx + lane * pitch;
   const int64_t tc_stride = d.tiles * d.c;
   const int tx_end = WIDE ? min(d.tw, tx0 + twb) : d.tw;
+  const int ntr = min(trows, d.th - ty0);
+  for (int tyl = 0; tyl < ntr; ++tyl)
   for (int tx = tx0 + warp; tx < tx_end; tx += nwarps) {
+    const int ty = ty0 + tyl;
     const int64_t tile = ((int64_t)n * d.th + ty) * d.tw + tx;
     T* vout = V + tile * d.c + c0 + lane;
     int fq = 0;
@@ -314,7 +332,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = 2 * ty + i;
-        const int rs = R.origin + d.s_h * i;  // staged-row index (rows outside x are staged zeros)
+        const int rs = R.origin + d.s_h * (i + 2 * tyl);  // staged-row index (rows outside x are staged zeros)
         rows[i] = (i < lr && k < d.oh - 1 + pr) ? rs * ws : -1;
       }
       for (int cp = 0; cp < d.n_col_parts; ++cp) {
@@ -329,11 +347,11 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
         }
         T* vq = vout + (int64_t)fq * tc_stride;
         if (check) {
-#define DWM_ITP(A, B) it_gather_part<A, B, true>(sc, rows, cols, vq, tc_stride)
+#define DWM_ITP(A, B) it_gather_part<A, B, true, STREAM>(sc, rows, cols, vq, tc_stride)
           DWM_PART_SWITCH(pr, pc, DWM_ITP)
 #undef DWM_ITP
         } else {
-#define DWM_ITP(A, B) it_gather_part<A, B, false>(sc, rows, cols, vq, tc_stride)
+#define DWM_ITP(A, B) it_gather_part<A, B, false, STREAM>(sc, rows, cols, vq, tc_stride)
           DWM_PART_SWITCH(pr, pc, DWM_ITP)
 #undef DWM_ITP
         }
@@ -388,17 +406,32 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
     smem = (size_t)IT_CB * ((size_t)rows * ws + 1) * sizeof(T);
   }
   const bool wide = twb != d.tw;
-  auto kern = wide ? input_transform_smem_kernel<T, true> : input_transform_smem_kernel<T, false>;
+  // whole rows: stage trows tile rows per CTA when they fit (the rows
+  // neighbouring tile rows share are loaded once, less CTA setup per tile)
+  int trows = 1;
+  if (!wide && d.num_freqs <= IT_TROWS_MAX_FREQS) {
+    const int rows_t = rows + (DWM_IT_TROWS - 1) * 2 * d.s_h;
+    const size_t smem_t = (size_t)IT_CB * ((size_t)rows_t * ws + 1) * sizeof(T);
+    if (DWM_IT_TROWS > 1 && smem_t <= CAP) {
+      trows = DWM_IT_TROWS;
+      rows = rows_t;
+      smem = smem_t;
+    }
+  }
+  const bool stream = d.num_freqs > IT_STREAM_MIN_FREQS;
+  auto kern = wide ? (stream ? input_transform_smem_kernel<T, true, true> : input_transform_smem_kernel<T, true, false>)
+                   : (stream ? input_transform_smem_kernel<T, false, true> : input_transform_smem_kernel<T, false, false>);
   DWM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int nxb = (d.tw + twb - 1) / twb;
-  const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)((int64_t)d.n * d.th * nxb));
+  const int nty = (d.th + trows - 1) / trows;
+  const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)((int64_t)d.n * nty * nxb));
   // warps: a divisor of the tile count in [4, 8] so every warp gets the same number of tiles
   int warps = 8;
   if (twb <= 8) warps = twb;
   else
     for (int cand = 8; cand >= 4; --cand)
       if (twb % cand == 0) { warps = cand; break; }
-  kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws);
+  kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows);
   DWM_CUDA_TRY(cudaGetLastError());
   *used = true;
   return DWM_OK;

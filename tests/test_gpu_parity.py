@@ -85,6 +85,26 @@ def test_input_transform_wide_rows_bit_exact(cuda, geom, dtype):
     assert np.array_equal(v, v_ref)
 
 
+@pytest.mark.parametrize("geom", [((3, 3), (1, 1), (1, 1, 1, 1), 40, 2, 9, 11),   # 5 tile rows: groups 4 + 1
+                                  ((3, 3), (1, 1), (0, 2, 1, 0), 64, 3, 14, 8),   # 7 tile rows, odd last row
+                                  ((3, 2), (1, 1), (1, 0, 0, 1), 33, 2, 16, 13),  # 8 tile rows, 1-channel tail block
+                                  ((2, 3), (1, 1), (0, 0, 1, 1), 32, 1, 6, 6)],   # 3 tile rows: one partial group
+                         ids=["3x3h9", "3x3h14odd", "3x2h16c33", "2x3h6"])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_input_transform_multi_tile_row_bit_exact(cuda, geom, dtype):
+    """Few-frequency plans stage several tile rows per CTA (DWM_IT_TROWS):
+    partial last groups, odd extents and ragged channel blocks keep V
+    bit-identical to the reference's."""
+    import torch
+    k, st, pad, c, n, h, w = geom
+    spec = ConvSpec(kernel=k, stride=st, pad=pad)
+    d = np.random.default_rng(h * w + c).standard_normal((n, c, h, w))
+    desc = _native.make_desc(n, c, h, w, 1, spec.kernel, spec.stride, spec.pad)
+    v_ref = input_transform_oracle(d, spec, dtype)
+    v = _stage(torch, _native.load().dwm_input_transform, desc, dtype, d.astype(dtype), v_ref.shape, cuda)
+    assert np.array_equal(v, v_ref)
+
+
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
 def test_exact_engine_matches_reference_golden(cuda, case):
     d, g = ARR[f"{case['name']}/data"], ARR[f"{case['name']}/weights"]
