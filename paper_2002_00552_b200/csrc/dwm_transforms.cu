@@ -209,9 +209,10 @@ constexpr int IT_STREAM_MIN_FREQS = 64;  // evict-first V stores above this many
 // many-frequency plans (V/x >= 25: cfg4 7x7 -9 %, 11x11 -7 %), slower for
 // 3x3 (+4 %: there the staged-row overlap between neighbouring tile rows is
 // re-read from L2), see DESIGN.md section 3.3.
-// UNITC (unit column stride, no CHECK): one row pointer per window row and
-// immediate column offsets instead of an address add per sample.
-template <int PR, int PC, bool CHECK, bool STREAM, bool UNITC, typename T>
+// CSTR = compile-time column stride s_w (1 or 2; 0 = runtime), no CHECK: one
+// row pointer per window row and immediate column offsets instead of an
+// address add per sample.
+template <int PR, int PC, bool CHECK, bool STREAM, int CSTR, typename T>
 __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const int (&rows)[4], const int (&cols)[4],
                                                T* vq, int64_t stride) {
   // the staged block is zero-padded, so only the even-extension truncation
@@ -219,10 +220,10 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
   T win[4][4];
 #pragma unroll
   for (int i = 0; i <= PR; ++i) {
-    if constexpr (UNITC && !CHECK) {
+    if constexpr (CSTR > 0 && !CHECK) {
       const T* r = sc + rows[i] + cols[0];
 #pragma unroll
-      for (int j = 0; j <= PC; ++j) win[i][j] = r[j];
+      for (int j = 0; j <= PC; ++j) win[i][j] = r[CSTR * j];
     } else {
 #pragma unroll
       for (int j = 0; j <= PC; ++j)
@@ -324,7 +325,6 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   if (lane >= cb) return;
   const T* sc = sx + lane * pitch;
   const int64_t tc_stride = d.tiles * d.c;
-  const bool unit_col = d.s_w == 1;
   const int tx_end = WIDE ? min(d.tw, tx0 + twb) : d.tw;
   const int ntr = min(trows, d.th - ty0);
   for (int tyl = 0; tyl < ntr; ++tyl)
@@ -357,17 +357,21 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
         }
         T* vq = vout + (int64_t)fq * tc_stride;
         if (check) {
-#define DWM_ITP(A, B) it_gather_part<A, B, true, STREAM, false>(sc, rows, cols, vq, tc_stride)
+#define DWM_ITP(A, B) it_gather_part<A, B, true, STREAM, 0>(sc, rows, cols, vq, tc_stride)
           DWM_PART_SWITCH(pr, pc, DWM_ITP)
 #undef DWM_ITP
         } else {
-#define DWM_ITP(A, B) it_gather_part<A, B, false, STREAM, false>(sc, rows, cols, vq, tc_stride)
-#define DWM_ITPU(A, B) it_gather_part<A, B, false, STREAM, true>(sc, rows, cols, vq, tc_stride)
-          if (unit_col) {
+#define DWM_ITP(A, B) it_gather_part<A, B, false, STREAM, 0>(sc, rows, cols, vq, tc_stride)
+#define DWM_ITPU(A, B) it_gather_part<A, B, false, STREAM, 1>(sc, rows, cols, vq, tc_stride)
+#define DWM_ITP2(A, B) it_gather_part<A, B, false, STREAM, 2>(sc, rows, cols, vq, tc_stride)
+          if (d.s_w == 1) {
             DWM_PART_SWITCH(pr, pc, DWM_ITPU)
+          } else if (d.s_w == 2) {
+            DWM_PART_SWITCH(pr, pc, DWM_ITP2)
           } else {
             DWM_PART_SWITCH(pr, pc, DWM_ITP)
           }
+#undef DWM_ITP2
 #undef DWM_ITPU
 #undef DWM_ITP
         }
