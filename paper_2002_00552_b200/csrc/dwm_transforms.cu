@@ -243,7 +243,7 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
 template <typename T, bool WIDE, bool STREAM>
 __global__ void __maxnreg__(DWM_IT_MAXNREG)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
-                            int twb_arg, int ws_arg, int trows_arg) {
+                            int twb_arg, int ws_arg, int trows_arg, int n0) {
   // WIDE == false: whole rows staged (ws == W, trows tile rows per CTA) -- the
   // common case, compiled without any of the column-block arithmetic
   const int twb = WIDE ? twb_arg : d.tw;
@@ -259,7 +259,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   const int tx0 = WIDE ? (int)(blockIdx.y % nxb) * twb : 0;
   const int nty = WIDE ? d.th : (d.th + trows - 1) / trows;
   const int ty0 = WIDE ? (int)(blockIdx.y / nxb) % d.th : (int)(blockIdx.y % nty) * trows;
-  const int n = WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / nty);
+  const int n = n0 + (WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / nty));  // image
   const int cbase = WIDE ? 2 * tx0 * d.s_w - d.pad_left : -d.pad_left;  // input column of staged column 0
   const int c0 = blockIdx.x * IT_CB;
   const int cb = min(IT_CB, d.c - c0);
@@ -438,21 +438,28 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
       smem = smem_t;
     }
   }
+  const int nxb = (d.tw + twb - 1) / twb;
+  const int nty = (d.th + trows - 1) / trows;
+  // grid.y = images x CTAs per image must stay <= 65535: launch batch slices
+  const int per_img = nty * nxb;
+  if (per_img > 65535) return DWM_OK;  // (never at BASELINE sizes) the 1-D-grid kernel takes it
+  const int imgs_per_launch = 65535 / per_img;
   const bool stream = d.num_freqs > IT_STREAM_MIN_FREQS;
   auto kern = wide ? (stream ? input_transform_smem_kernel<T, true, true> : input_transform_smem_kernel<T, true, false>)
                    : (stream ? input_transform_smem_kernel<T, false, true> : input_transform_smem_kernel<T, false, false>);
   DWM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int nxb = (d.tw + twb - 1) / twb;
-  const int nty = (d.th + trows - 1) / trows;
-  const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)((int64_t)d.n * nty * nxb));
   // warps: a divisor of the tile count in [4, 8] so every warp gets the same number of tiles
   int warps = 8;
   if (twb <= 8) warps = twb;
   else
     for (int cand = 8; cand >= 4; --cand)
       if (twb % cand == 0) { warps = cand; break; }
-  kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows);
-  DWM_CUDA_TRY(cudaGetLastError());
+  for (int n0 = 0; n0 < d.n; n0 += imgs_per_launch) {
+    const int nb = min(imgs_per_launch, d.n - n0);
+    const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)(nb * per_img));
+    kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows, n0);
+    DWM_CUDA_TRY(cudaGetLastError());
+  }
   *used = true;
   return DWM_OK;
 }

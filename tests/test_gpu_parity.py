@@ -85,6 +85,31 @@ def test_input_transform_wide_rows_bit_exact(cuda, geom, dtype):
     assert np.array_equal(v, v_ref)
 
 
+def test_input_transform_batch_beyond_grid_y_limit(cuda):
+    """70000 images x 1 CTA row each exceeds the 65535 grid.y limit: the
+    launcher slices the batch; the last images' V equals a run on them alone."""
+    import torch
+    spec = ConvSpec(kernel=(3, 3), stride=(1, 1), pad=(1, 1, 1, 1))
+    n, c, h, w = 70000, 32, 4, 4
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    x = torch.randn(n, c, h, w, device=cuda, generator=gen)
+    lib = _native.load()
+
+    def run(xs):
+        desc = _native.make_desc(xs.shape[0], c, h, w, 1, spec.kernel, spec.stride, spec.pad)
+        v = torch.full((desc.num_freqs, desc.tiles, c), float("nan"), device=cuda)
+        _native.check(lib.dwm_input_transform(desc, _native.DWM_F32, xs.data_ptr(), v.data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream))
+        return v
+
+    v_all = run(x)
+    tail = 7
+    v_tail = run(x[n - tail:].contiguous())
+    per = v_tail.shape[1] // tail
+    assert torch.equal(v_all[:, (n - tail) * per:], v_tail)
+    assert not torch.isnan(v_all).any()
+
+
 @pytest.mark.parametrize("geom", [((3, 3), (1, 1), (1, 1, 1, 1), 40, 2, 9, 11),   # 5 tile rows: groups 4 + 1
                                   ((3, 3), (1, 1), (0, 2, 1, 0), 64, 3, 14, 8),   # 7 tile rows, odd last row
                                   ((3, 2), (1, 1), (1, 0, 0, 1), 33, 2, 16, 13),  # 8 tile rows, 1-channel tail block
