@@ -381,8 +381,14 @@ int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void*
       // small problem (e.g. one 56x56 image): one output per thread, 16x16
       // blocks, so the work spreads over the SMs instead of a handful of CTAs
       constexpr int SB = 16;
+#ifndef DWM_EXACT_SMALL_KC
+#define DWM_EXACT_SMALL_KC 32
+#endif
+      // deeper K chunks: each chunk is a load -> barrier -> FMA round trip,
+      // which is what bounds a problem this small (same summation order)
+      constexpr int SKC = DWM_EXACT_SMALL_KC;
       const dim3 g2((unsigned)((d.tiles + SB - 1) / SB), (unsigned)((d.f + SB - 1) / SB));
-      gemm_exact_kernel<float, SB, SB, 1, 1, KC><<<g2, SB * SB, 0, s>>>(
+      gemm_exact_kernel<float, SB, SB, 1, 1, SKC><<<g2, SB * SB, 0, s>>>(
           d, (const float*)V, (const float*)U, (float*)y, flag);
     } else {
       const dim3 grid((unsigned)((d.tiles + BM - 1) / BM), (unsigned)((d.f + BN - 1) / BN));
