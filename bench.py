@@ -1,26 +1,41 @@
 #!/usr/bin/env python
-"""Benchmark: DWM conv2d forward on B200 (images/s, direct-equivalent TFLOP/s).
+"""Benchmark: DWM conv2d forward on B200 (images/s, direct-equivalent TFLOP/s,
+MSE vs an FP64 direct convolution).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
-                    [--algo auto|exact|tc] [--impl b200|reference]
+                    [--algo auto|exact|tc|small_c] [--impl b200|reference]
+                    [--scaling weak|strong]
 
 One step = one full DWM conv2d forward (filter transform, input transform,
-transform-domain contraction with the fused output transform) over one
-batch of the workload (BASELINE.json configs; default configs[1], the
-ResNet-50 stem 7x7/s2 3->64 224x224 batch 256).  Multi-GPU: one process per
-GPU (torchrun), every rank runs the full per-GPU batch (weak scaling; images
-are independent so there is no collective on the forward path), timed on the
-device with CUDA events, max over ranks.
+transform-domain contraction with the fused output transform) over one batch
+of the workload (BASELINE.json configs).  The default is the headline sweep's
+largest single-GPU configuration, cfg4 11x11 stride 1, 256->256, 28x28,
+batch 512 (configs[3]: "batch 512 sharded over 1/2/4/8 GPUs"), which runs on
+the tcgen05 engine.
 
-``--impl reference`` times the reference's CPU algorithm (the NumPy port in
-oracle/, bit-identical to the reference in the build container) on this
-host's cores on a bounded slice of the same workload.
+Multi-GPU: one process per GPU.  ``--gpus N`` without a torchrun environment
+re-launches itself under ``torch.distributed.run`` (127.0.0.1).  cfg4/cfg5
+default to strong scaling (the workload's batch is sharded over the ranks,
+as BASELINE.json states); images are independent, so the forward path has
+no collective.  Every rank is timed on the device with CUDA events; the job
+time is the max over ranks.
+
+Accuracy: image 0 of the timed batch and the weights are the reference
+harness's draw (``pkg/src/dwmconv/bench.py:103-109``, seed 1, batch 1); after
+the timed region that image's output is compared with a binary64 direct
+convolution computed here, and with the reference DWM32 MSE on the same
+draw (tests/golden/baseline_samples.json, generated from the reference).
+
+``--impl reference`` times the reference's own CPU implementation
+(``dwmconv.engines.dwm_conv2d``, installed unmodified into baseline/_ref;
+the bit-identical NumPy port in oracle/ when that is absent) on this host's
+cores, on bounded slices of the same workload.
 """
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,26 +51,58 @@ sys.path.insert(0, str(ROOT))
 BASELINE_METRIC = "DWM conv2d images/s & equiv TFLOP/s at 1/2/4/8 B200; MSE vs FP64 direct conv"
 L2_BYTES = 126 * 2 ** 20
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
-def parse():
+def parse(argv=None):
     from paper_2002_00552_b200.configs import DEFAULT_WORKLOAD, WORKLOADS
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--algo", default="auto", choices=["auto", "exact", "tc", "small_c"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--batch", type=int, default=None, help="override per-GPU batch (debug only)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank runs the workload's batch; strong: the batch is sharded over ranks")
+    ap.add_argument("--batch", type=int, default=None, help="override the global batch (debug only)")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="strong: the workload's batch is sharded over the ranks (default for cfg4/cfg5); "
+                         "weak: every rank runs the workload's batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args()
+    ap.add_argument("--no-check", action="store_true", help="skip the sampled-image MSE check")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo dry run of the launch, sharding and timing logic with the kernel call "
+                         "stubbed (tests only; prints a line marked dry_run)")
+    return ap.parse_args(argv)
 
 
+def default_scaling(wl) -> str:
+    return "strong" if wl.name.startswith(("cfg4", "cfg5")) else "weak"
+
+
+# ---------------------------------------------------------------------------
+# self-launch under torchrun for --gpus N
+# ---------------------------------------------------------------------------
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args) -> int:
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "4"))
+    return subprocess.call(cmd, env=env)
+
+
+# ---------------------------------------------------------------------------
+# peaks
+# ---------------------------------------------------------------------------
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -161,22 +208,56 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU arms (oracle = NumPy port of the reference, bit-identical in the build
-# container); only used as the reported baseline / the reference arm.
+# inputs and the accuracy check (reference harness recipe, restated)
 # ---------------------------------------------------------------------------
-def cpu_reference_rate(wl, seconds: float, images_per_rep: int = 2, min_reps: int = 2):
+def draw(seed: int, kernel, stride, hw: int, channels: int, filters: int, batch: int):
+    """N(0,1) float64 data then weights from one PCG64 stream keyed on the
+    config -- the reference accuracy harness's ``_draw`` (bench.py:103-109)."""
+    entropy = [seed, *kernel, *stride, hw, channels, filters, batch]
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy)))
+    data = rng.standard_normal((batch, channels, hw, hw))
+    weights = rng.standard_normal((filters, channels, *kernel))
+    return data, weights
+
+
+def direct_f64(x: np.ndarray, w: np.ndarray, spec) -> np.ndarray:
+    """Binary64 strided cross-correlation of one image (im2col + one BLAS
+    matmul) -- the ground truth of the reference harness (bench.py:134)."""
+    c, h, wd = x.shape
+    f = w.shape[0]
+    (r_h, r_w), (s_h, s_w) = spec.kernel, spec.stride
+    top, bottom, left, right = spec.pad
+    oh, ow = spec.out_dims(h, wd)
+    xp = np.zeros((c, h + top + bottom, wd + left + right))
+    xp[:, top:top + h, left:left + wd] = x
+    cols = np.lib.stride_tricks.sliding_window_view(xp, (r_h, r_w), axis=(1, 2))[:, ::s_h, ::s_w][:, :oh, :ow]
+    cols = cols.transpose(0, 3, 4, 1, 2).reshape(c * r_h * r_w, oh * ow)
+    return (w.reshape(f, -1).astype(np.float64) @ cols).reshape(f, oh, ow)
+
+
+def golden_reference_mse(wl):
+    p = ROOT / "tests" / "golden" / "baseline_samples.json"
+    try:
+        return json.loads(p.read_text())[wl.name]["dwm32_mse"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference's own implementation (baseline/_ref), else the oracle port
+# ---------------------------------------------------------------------------
+def reference_impl():
+    """(dwm_conv2d, ConvSpec, kind, description) of the CPU reference: the
+    unmodified reference package from baseline/_ref, or the oracle port."""
+    if (REF_DIR / "dwmconv" / "__init__.py").exists():
+        sys.path.insert(0, str(REF_DIR))
+        sys.dont_write_bytecode = True
+        from dwmconv import ConvSpec as RefSpec
+        from dwmconv.engines import dwm_conv2d as ref_dwm
+        return ref_dwm, RefSpec, "reference", "dwmconv.engines.dwm_conv2d (reference, baseline/_ref)"
     from oracle.dwm_oracle import dwm_conv2d_oracle
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal((images_per_rep, wl.c_in, wl.hw, wl.hw)).astype(np.float32)
-    w = rng.standard_normal((wl.c_out, wl.c_in, wl.kernel, wl.kernel)).astype(np.float32)
-    spec = wl.spec()
-    dwm_conv2d_oracle(x, w, spec)  # warm (BLAS threads, page-in)
-    reps, t0 = 0, time.perf_counter()
-    while reps < min_reps or time.perf_counter() - t0 < seconds:
-        dwm_conv2d_oracle(x, w, spec)
-        reps += 1
-    dt = time.perf_counter() - t0
-    return images_per_rep * reps / dt, reps, dt
+    from paper_2002_00552_b200 import ConvSpec
+    return dwm_conv2d_oracle, ConvSpec, "port", "oracle/dwm_oracle.py (bit-identical NumPy port)"
 
 
 def cpu_threads():
@@ -196,49 +277,266 @@ def cpu_model():
     return "unknown"
 
 
-def run_reference_arm(args, wl, rank):
+def cpu_reference_rate(wl, seconds: float):
+    """Images/s of the CPU reference on slices of 1 and 2 images (linearity
+    check), best of the repetitions that fit in ``seconds``."""
+    fn, Spec, kind, what = reference_impl()
+    spec = Spec(kernel=(wl.kernel, wl.kernel), stride=(wl.stride, wl.stride), pad=(wl.pad,) * 4)
+    rng = np.random.default_rng(0)
+    w = rng.standard_normal((wl.c_out, wl.c_in, wl.kernel, wl.kernel)).astype(np.float32)
+    rates = {}
+    t_end = time.perf_counter() + seconds
+    for n in (1, 2):
+        x = rng.standard_normal((n, wl.c_in, wl.hw, wl.hw)).astype(np.float32)
+        fn(x, w, spec)  # warm (BLAS threads, page-in)
+        best = None
+        reps = 0
+        while reps < 2 or (time.perf_counter() < t_end and reps < 20):
+            t0 = time.perf_counter()
+            fn(x, w, spec)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+            reps += 1
+            if n == 1 and time.perf_counter() > t_end - seconds / 2:
+                break
+        rates[n] = n / best
+    return rates, kind, what
+
+
+def run_reference_arm(args, wl, rank, world):
     if rank != 0:
         return
-    from oracle.dwm_oracle import dwm_conv2d_oracle
-    images = 2
+    fn, Spec, kind, what = reference_impl()
+    spec = Spec(kernel=(wl.kernel, wl.kernel), stride=(wl.stride, wl.stride), pad=(wl.pad,) * 4)
+    # each step is a bounded slice of the workload's batch (images are independent)
+    images = 1 if wl.direct_flops_per_image() > 2e9 else 2
     rng = np.random.default_rng(0)
     x = rng.standard_normal((images, wl.c_in, wl.hw, wl.hw)).astype(np.float32)
     w = rng.standard_normal((wl.c_out, wl.c_in, wl.kernel, wl.kernel)).astype(np.float32)
-    spec = wl.spec()
     for _ in range(args.warmup):
-        dwm_conv2d_oracle(x, w, spec)
+        fn(x, w, spec)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        dwm_conv2d_oracle(x, w, spec)
+        fn(x, w, spec)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = images * args.steps / total
     cores = cpu_threads()
-    sample = (f"{images} images of {wl.name} per step (the reference's NumPy DWM algorithm, "
-              f"oracle/dwm_oracle.py port, OpenBLAS {cores} threads, {cpu_model()})")
+    sample = (f"{images} image(s) of {wl.name} per step: {what}, float32, "
+              f"OpenBLAS {cores} threads, {cpu_model()}")
+    scaling = args.scaling or default_scaling(wl)
     line = {
         "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": "images/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1)",
-        "config": {"workload": wl.name, "kernel": wl.kernel, "stride": wl.stride, "pad": wl.pad,
-                   "hw": wl.hw, "c_in": wl.c_in, "c_out": wl.c_out, "batch_per_step": images},
+        "config": workload_config(wl, None, images, images, None, None),
         "equiv_tflops": value * wl.direct_flops_per_image() / 1e12,
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def workload_config(wl, desc, batch, global_batch, engine, world):
+    cfg = {"workload": wl.name, "kernel": wl.kernel, "stride": wl.stride, "pad": wl.pad,
+           "hw": wl.hw, "c_in": wl.c_in, "c_out": wl.c_out, "batch_per_gpu": batch,
+           "global_batch": global_batch}
+    if desc is not None:
+        cfg.update({"out_hw": [desc.oh, desc.ow], "parts": desc.n_row_parts * desc.n_col_parts,
+                    "frequencies": desc.num_freqs, "engine": engine,
+                    "parallelism": f"batch-sharded x{world}, no forward collective"})
+    return cfg
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+class GpuRunner:
+    """Device buffers and the timed step for one rank's shard."""
+
+    def __init__(self, args, wl, batch, dev):
+        import torch
+        from paper_2002_00552_b200 import _native
+        self.torch, self._native = torch, _native
+        self.lib = _native.load()
+        self.wl, self.batch, self.dev = wl, batch, dev
+        self.spec = wl.spec()
+        self.desc = _native.make_desc(batch, wl.c_in, wl.hw, wl.hw, wl.c_out, self.spec.kernel,
+                                      self.spec.stride, self.spec.pad)
+        self.algo = _native.ALGOS[args.algo]
+        sel = self.lib.dwm_select_algo(self.desc, _native.DWM_F32, self.algo)
+        if sel < 0:
+            raise SystemExit(f"engine {args.algo} is not available for {wl.name}")
+        self.engine = _native.ALGO_NAMES[sel]
+        self.ws_bytes = self.lib.dwm_workspace_bytes(self.desc, _native.DWM_F32, self.algo)
+        # image 0 and the weights: the reference harness draw (seed 1, batch 1)
+        d0, w0 = draw(1, (wl.kernel, wl.kernel), (wl.stride, wl.stride), wl.hw, wl.c_in, wl.c_out, 1)
+        self.x0, self.w0 = d0[0], w0
+        gen = torch.Generator(device=dev).manual_seed(1234)
+        self.x = torch.randn(batch, wl.c_in, wl.hw, wl.hw, device=dev, generator=gen)
+        self.x[0].copy_(torch.from_numpy(d0[0].astype(np.float32)))
+        self.w = torch.from_numpy(w0.astype(np.float32)).to(dev)
+        self.y = torch.empty(batch, wl.c_out, self.desc.oh, self.desc.ow, device=dev)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.stream = torch.cuda.current_stream(dev)
+        self.sptr = self.stream.cuda_stream
+        d = self.desc
+        self.x_bytes, self.w_bytes, self.y_bytes = self.x.numel() * 4, self.w.numel() * 4, self.y.numel() * 4
+        self.v_bytes = 0 if self.engine == "small_c" else d.num_freqs * d.tiles * wl.c_in * 4
+        self.u_bytes = d.num_freqs * wl.c_out * wl.c_in * 4 * (2 if self.engine == "tc" else 1)
+        self.working_set = self.x_bytes + self.y_bytes + self.v_bytes
+        self.flush = (torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+                      if self.working_set < 4 * L2_BYTES else None)
+        self.launches_per_step = 2 if self.engine == "small_c" else 3
+
+    def step(self):
+        st = self.lib.dwm_conv2d_forward(self.desc, self._native.DWM_F32, self.algo, self.x.data_ptr(),
+                                         self.w.data_ptr(), self.y.data_ptr(), self.ws.data_ptr(),
+                                         self.ws_bytes, self.flag.data_ptr(), self.sptr)
+        if st:
+            self._native.check(st, "dwm_conv2d_forward")
+
+    def warm(self, n):
+        for _ in range(n):
+            self.step()
+        self.torch.cuda.synchronize()
+        if int(self.flag.item()):
+            raise FloatingPointError("dwm_conv2d produced non-finite values")
+
+    def timed(self, steps):
+        """Per-step CUDA-event times (ms) on the launching stream."""
+        torch = self.torch
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        torch.cuda.synchronize()
+        for i in range(steps):
+            if self.flush is not None:
+                self.flush.zero_()
+            starts[i].record(self.stream)
+            self.step()
+            ends[i].record(self.stream)
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+    def check_sample(self):
+        """MSE of image 0 of the timed batch vs a binary64 direct conv."""
+        if int(self.flag.item()):
+            raise FloatingPointError("dwm_conv2d produced non-finite values in the timed region")
+        y0 = self.y[0].double().cpu().numpy()
+        # ground truth on the binary64 draw, as the reference harness does
+        # (bench.py:134: direct_conv2d(data, weights, precision=float64))
+        ref = direct_f64(self.x0, self.w0, self.spec)
+        err = float(np.mean((y0 - ref) ** 2))
+        gold = golden_reference_mse(self.wl)
+        out = {"image": 0, "mse_vs_fp64": err, "reference_dwm32_mse": gold,
+               "mse_ratio_vs_reference": (err / gold) if gold else None,
+               "max_abs_err": float(np.max(np.abs(y0 - ref))),
+               "recipe": "reference bench.py:103-109 draw, seed 1, batch 1 (image 0 + weights); "
+                         "reference DWM32 MSE from tests/golden/baseline_samples.json"}
+        return out
+
+    def stage_times(self, reps):
+        """Median CUDA-event time of each kernel of the step, run alone."""
+        torch, lib, F32 = self.torch, self.lib, self._native.DWM_F32
+        check = self._native.check
+        V = self.ws.data_ptr()
+        U = V + ((self.v_bytes + 255) // 256) * 256
+        d = self.desc
+
+        def filt():
+            check(lib.dwm_prepare_filter(d, F32, self.algo, self.w.data_ptr(), U, self.sptr))
+
+        def inp():
+            check(lib.dwm_input_transform(d, F32, self.x.data_ptr(), V, self.sptr))
+
+        def gemm():
+            check(lib.dwm_gemm_output(d, F32, self.algo, V, U, self.y.data_ptr(), self.flag.data_ptr(),
+                                      None, 0, self.sptr))
+
+        def small_c():
+            check(lib.dwm_conv2d_small_c(d, self.x.data_ptr(), U, self.y.data_ptr(), self.flag.data_ptr(),
+                                         self.sptr))
+
+        self.step()  # V/U hold the engine's (layout-specific) contents
+        if self.engine == "small_c":
+            names = [("filter_transform", filt), ("conv2d_small_c", small_c)]
+        else:
+            names = [("filter_transform", filt), ("input_transform", inp), ("gemm_output", gemm)]
+        out = {}
+        for name, fn in names:
+            ms = []
+            for _ in range(reps):
+                if self.flush is not None:
+                    self.flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(self.stream)
+                fn()
+                b.record(self.stream)
+                torch.cuda.synchronize()
+                ms.append(a.elapsed_time(b))
+            out[name] = statistics.median(ms)
+        return out
+
+    def e2e(self, steps, dist, world, barrier):
+        """Public-API call with pinned HOST buffers: H2D of x and w, the
+        forward, D2H of y and of the non-finite flag, every step."""
+        torch = self.torch
+        from paper_2002_00552_b200 import dwm_conv2d
+        wl = self.wl
+        xh = torch.randn(self.batch, wl.c_in, wl.hw, wl.hw).pin_memory()
+        wh = self.w.cpu().pin_memory()
+        yh = torch.empty(self.batch, wl.c_out, self.desc.oh, self.desc.ow).pin_memory()
+        for _ in range(2):
+            dwm_conv2d(xh, wh, self.spec, out=yh)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            dwm_conv2d(xh, wh, self.spec, out=yh)
+        torch.cuda.synchronize()
+        from paper_2002_00552_b200.sharding import max_over_ranks
+        dt = max_over_ranks(time.perf_counter() - t0, dist, self.dev)
+        return dt, {"h2d_bytes_per_step": (xh.numel() + wh.numel()) * 4, "d2h_bytes_per_step": yh.numel() * 4 + 4,
+                    "steps": steps,
+                    "path": "paper_2002_00552_b200.dwm_conv2d(pinned host tensors, out=pinned host tensor)"}
+
+
+class DryRunner:
+    """CPU stand-in for GpuRunner (tests): same sharding/timing/launch logic,
+    the kernel call is stubbed and records the shard it was given."""
+
+    def __init__(self, args, wl, batch, dev):
+        from paper_2002_00552_b200.convspec import ConvSpec  # noqa: F401
+        self.wl, self.batch = wl, batch
+        self.spec = wl.spec()
+        self.engine = "dry_run"
+        self.desc = None
+        self.flush = None
+        self.working_set = 0
+        self.launches_per_step = 0
+        self.calls = 0
+
+    def warm(self, n):
+        self.calls += n
+
+    def timed(self, steps):
+        out = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            self.calls += 1
+            out.append(1e3 * (time.perf_counter() - t0) + 1.0)
+        return out
+
+
 def main():
     args = parse()
     from paper_2002_00552_b200.configs import WORKLOADS
     wl = WORKLOADS[args.workload]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -248,99 +546,78 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = "nccl" if (torch.cuda.is_available() and not args.dry_run) else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local_rank)
         dist.init_process_group(backend=backend)
 
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
     if args.impl == "reference":
-        run_reference_arm(args, wl, rank)
+        run_reference_arm(args, wl, rank, world)
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    from paper_2002_00552_b200 import _native, dwm_conv2d
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    lib = _native.load()
     from paper_2002_00552_b200.sharding import max_over_ranks, shard_range
+    scaling = args.scaling or default_scaling(wl)
     global_batch = args.batch or wl.batch
-    if args.scaling == "strong":
+    if scaling == "strong":
         lo, hi = shard_range(global_batch, rank, world)
         batch = hi - lo
+        job_images = global_batch
     else:
         batch = global_batch
-    spec = wl.spec()
-    desc = _native.make_desc(batch, wl.c_in, wl.hw, wl.hw, wl.c_out, spec.kernel, spec.stride, spec.pad)
-    algo = _native.ALGOS[args.algo]
-    sel = lib.dwm_select_algo(desc, _native.DWM_F32, algo)
-    algo_name = _native.ALGO_NAMES.get(sel, "?")
-    ws_bytes = lib.dwm_workspace_bytes(desc, _native.DWM_F32, algo)
+        job_images = global_batch * world
 
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn(batch, wl.c_in, wl.hw, wl.hw, device=dev, generator=gen)
-    w = torch.randn(wl.c_out, wl.c_in, wl.kernel, wl.kernel, device=dev, generator=gen)
-    y = torch.empty(batch, wl.c_out, desc.oh, desc.ow, device=dev)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    sptr = stream.cuda_stream
+    if args.dry_run:
+        dev = torch.device("cpu")
+        run = DryRunner(args, wl, batch, dev)
+    else:
+        dev = torch.device("cuda", local_rank)
+        torch.cuda.set_device(dev)
+        run = GpuRunner(args, wl, batch, dev)
 
-    x_bytes, w_bytes, y_bytes = x.numel() * 4, w.numel() * 4, y.numel() * 4
-    v_bytes = 0 if algo_name == "small_c" else desc.num_freqs * desc.tiles * wl.c_in * 4
-    u_bytes = desc.num_freqs * wl.c_out * wl.c_in * 4 * (2 if algo_name == "tc" else 1)
-    working_set = x_bytes + y_bytes + v_bytes
-    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if working_set < 4 * L2_BYTES else None
+    clocks = ClockSampler(local_rank).__enter__() if not args.dry_run else None
+    if clocks is not None:
+        clocks.wait_first()
+    warmup = max(args.warmup, 3)
+    run.warm(warmup)
 
-    def step():
-        st = lib.dwm_conv2d_forward(desc, _native.DWM_F32, algo, x.data_ptr(), w.data_ptr(), y.data_ptr(),
-                                    ws.data_ptr(), ws_bytes, flag.data_ptr(), sptr)
-        if st:
-            _native.check(st, "dwm_conv2d_forward")
+    # ---- timed region: K steps, barrier + synchronize on both sides, max over ranks
+    barrier()
+    n_before = len(clocks.lines) if clocks else 0
+    step_ms = run.timed(args.steps)
+    if clocks is not None:
+        time.sleep(0.06)
+        clocks.__exit__(None, None, None)
+        if len(clocks.lines) - n_before >= 3:
+            clocks.lines = clocks.lines[n_before:]
+    barrier()
+    total_ms = max_over_ranks(sum(step_ms), dist, dev if not args.dry_run else None)
+    value = job_images * args.steps / (total_ms / 1e3)
 
-    clocks = ClockSampler(dev.index).__enter__()
-    clocks.wait_first()
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    if int(flag.item()):
-        raise FloatingPointError("dwm_conv2d produced non-finite values")
+    if args.dry_run:
+        calls = max_over_ranks(float(run.calls), dist)
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "metric": BASELINE_METRIC, "value": value, "unit": "images/s",
+                              "n_gpus": world, "steps": args.steps, "warmup": warmup, "scaling": scaling,
+                              "config": workload_config(wl, None, batch, job_images, None, world),
+                              "shard": [lo, hi] if scaling == "strong" else [0, batch],
+                              "calls": int(calls)}), flush=True)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
 
-    # ---- timed region: K steps, per-step CUDA events on the launching stream
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    n_before = len(clocks.lines)
-    if True:
-        for i in range(args.steps):
-            if flush is not None:
-                flush.zero_()
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-    time.sleep(0.06)
-    clocks.__exit__(None, None, None)
-    # samples from the warm-up on; keep the timed-region ones when there are enough
-    if len(clocks.lines) - n_before >= 3:
-        clocks.lines = clocks.lines[n_before:]
-    if dist is not None:
-        dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = max_over_ranks(sum(step_ms), dist, dev)
-    images = (global_batch if args.scaling == "strong" else batch * world) * args.steps
-    value = images / (total_ms / 1e3)
-    launches_per_step = 2 if algo_name == "small_c" else 3
-
-    # ---- per-stage kernel times (same stream, CUDA events, after the timed region)
-    stage_ms = stage_times(lib, desc, algo, algo_name, x, w, y, ws, flag, sptr, stream, flush, reps=max(3, args.steps))
-
-    # ---- end-to-end through the public API with host buffers
+    sample = None if args.no_check or rank != 0 else run.check_sample()
+    stage_ms = run.stage_times(reps=max(3, min(args.steps, 10)))
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, wl, spec, batch, dev, dist, world, dwm_conv2d)
+        steps_e2e = max(2, min(args.steps, 5))
+        dt, info = run.e2e(steps_e2e, dist, world, barrier)
+        e2e = {"value": job_images * steps_e2e / dt, "unit": "images/s", **info}
 
     if rank != 0:
         if dist is not None:
@@ -348,136 +625,87 @@ def main():
         return
 
     peaks = load_peaks()
-    roofline, kernels = make_roofline(stage_ms, desc, wl, batch, algo_name, peaks,
-                                      x_bytes, w_bytes, y_bytes, v_bytes, u_bytes)
+    roofline, kernels = make_roofline(stage_ms, run, peaks)
     line = {
         "metric": BASELINE_METRIC, "value": value, "unit": "images/s",
-        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) (torch.randn on device)",
-        "config": {"workload": wl.name, "kernel": wl.kernel, "stride": wl.stride, "pad": wl.pad,
-                   "hw": wl.hw, "c_in": wl.c_in, "c_out": wl.c_out, "batch_per_gpu": batch,
-                   "global_batch": global_batch if args.scaling == "strong" else batch * world,
-                   "out_hw": [desc.oh, desc.ow],
-                   "parts": desc.n_row_parts * desc.n_col_parts, "frequencies": desc.num_freqs,
-                   "engine": algo_name,
-                   "l2": ("inputs+intermediates > L2 (%.2f GB/step)" % (working_set / 1e9)
-                          if flush is None else "L2 flushed between timed steps (256 MB write)"),
-                   "parallelism": f"batch-sharded x{world}, no forward collective"},
+        "n_gpus": world, "steps": args.steps, "warmup": warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1): image 0 + weights = reference harness draw (seed 1), other images torch.randn",
+        "config": dict(workload_config(wl, run.desc, batch, job_images, run.engine, world),
+                       l2=("inputs+intermediates > L2 (%.2f GB/step per GPU)" % (run.working_set / 1e9)
+                           if run.flush is None else "L2 flushed between timed steps (256 MB write)")),
         "equiv_tflops": value * wl.direct_flops_per_image() / 1e12,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": run.launches_per_step * args.steps,
         "clocks": clocks.summary(),
+        "accuracy": sample,
         "roofline": roofline,
         "kernels": kernels,
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world == 1:
-        rate, reps, dt = cpu_reference_rate(wl, args.cpu_seconds)
+        rates, kind, what = cpu_reference_rate(wl, args.cpu_seconds)
         line["cpu_baseline"] = {
-            "value": rate, "unit": "images/s", "cores": cpu_threads(), "kind": "port",
-            "sample": (f"{2 * reps} images of {wl.name} in {dt:.1f}s: reference NumPy DWM algorithm "
-                       f"(oracle/dwm_oracle.py, bit-identical port), OpenBLAS threads, {cpu_model()}")}
+            "value": max(rates.values()), "unit": "images/s", "cores": cpu_threads(), "kind": kind,
+            "sample": (f"best-of-reps slices of 1 and 2 images of {wl.name} ({rates[1]:.3g} / {rates[2]:.3g} "
+                       f"images/s: per-image linear), {what}, float32, OpenBLAS threads, {cpu_model()}")}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
 
-def stage_times(lib, desc, algo, algo_name, x, w, y, ws, flag, sptr, stream, flush, reps):
-    """Median CUDA-event time of each kernel the forward launches, run alone."""
-    import torch
-    from paper_2002_00552_b200 import _native
-    ws_ptr = ws.data_ptr()
-    v_bytes = 0 if algo_name == "small_c" else desc.num_freqs * desc.tiles * desc.c * 4
-    V = ws_ptr
-    U = ws_ptr + ((v_bytes + 255) // 256) * 256
-    F32 = _native.DWM_F32
-
-    def filt():
-        _native.check(lib.dwm_filter_transform(desc, F32, w.data_ptr(), U, sptr))
-
-    def inp():
-        _native.check(lib.dwm_input_transform(desc, F32, x.data_ptr(), V, sptr))
-
-    def gemm():
-        _native.check(lib.dwm_gemm_output(desc, F32, algo, V, U, y.data_ptr(), flag.data_ptr(),
-                                          None, 0, sptr))
-
-    def small_c():
-        _native.check(lib.dwm_conv2d_small_c(desc, x.data_ptr(), U, y.data_ptr(), flag.data_ptr(), sptr))
-
-    # one full forward so V/U hold the engine's (layout-specific) contents
-    _native.check(lib.dwm_conv2d_forward(desc, F32, algo, x.data_ptr(), w.data_ptr(), y.data_ptr(),
-                                         ws_ptr, ws.numel(), flag.data_ptr(), sptr))
-    if algo_name == "small_c":
-        names = [("filter_transform", filt), ("conv2d_small_c", small_c)]
-    elif algo_name == "tc":
-        names = [("input_transform", inp), ("gemm_output", gemm)]
-    else:
-        names = [("filter_transform", filt), ("input_transform", inp), ("gemm_output", gemm)]
-    out = {}
-    for name, fn in names:
-        ms = []
-        for _ in range(reps):
-            if flush is not None:
-                flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            ms.append(a.elapsed_time(b))
-        out[name] = statistics.median(ms)
-    return out
-
-
-def make_roofline(stage_ms, desc, wl, batch, algo_name, peaks, x_bytes, w_bytes, y_bytes, v_bytes, u_bytes):
+def make_roofline(stage_ms, run, peaks):
+    desc, engine = run.desc, run.engine
     hbm = peaks["hbm_gbs"]
     gemm_flops = 2.0 * desc.c * desc.f * desc.tiles * desc.num_freqs
-    kernels = []
     alg_bytes = {
-        "filter_transform": w_bytes + u_bytes,
-        "input_transform": x_bytes + v_bytes,
-        "gemm_output": v_bytes + u_bytes + y_bytes,
-        "conv2d_small_c": x_bytes + u_bytes + y_bytes,
+        "filter_transform": run.w_bytes + run.u_bytes,
+        "input_transform": run.x_bytes + run.v_bytes,
+        "gemm_output": run.v_bytes + run.u_bytes + run.y_bytes,
+        "conv2d_small_c": run.x_bytes + run.u_bytes + run.y_bytes,
     }
+    total = sum(stage_ms.values())
+    kernels = []
     for name, ms in stage_ms.items():
-        k = {"name": name, "ms": ms, "alg_bytes": alg_bytes[name],
-             "achieved_gbs": alg_bytes[name] / (ms * 1e-3) / 1e9}
+        k = {"name": name, "ms": ms, "share": ms / total, "alg_bytes": alg_bytes[name],
+             "achieved_gbs": alg_bytes[name] / (ms * 1e-3) / 1e9,
+             "hbm_frac": alg_bytes[name] / (ms * 1e-3) / 1e9 / hbm}
         if name in ("gemm_output", "conv2d_small_c"):
             k["dwm_gemm_flops"] = gemm_flops
             k["achieved_tflops"] = gemm_flops / (ms * 1e-3) / 1e12
+        if name == "gemm_output" and engine == "tc":
+            k["tensor_tflops_3xtf32"] = 3 * gemm_flops / (ms * 1e-3) / 1e12
+            k["tensor_frac"] = k["tensor_tflops_3xtf32"] / peaks["tf32_tflops"]
+        if name == "conv2d_small_c":
+            k["fp32_tflops"] = small_c_fp32_ops(desc) / (ms * 1e-3) / 1e12
+            k["fp32_frac"] = k["fp32_tflops"] / peaks["fp32_tflops"]
+        k["traffic"] = lookup_traffic(run.wl.name, name, run.batch)
         kernels.append(k)
-    total = sum(stage_ms.values())
-    for k in kernels:
-        k["share"] = k["ms"] / total
     top = max(kernels, key=lambda k: k["ms"])
-    traffic = lookup_traffic(wl.name, top["name"], batch)
-    if top["name"] == "gemm_output" and algo_name == "tc":
-        peak_tf32 = peaks["tf32_tflops"]
-        achieved = 3 * gemm_flops / (top["ms"] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": top["name"], "achieved": achieved,
-                "peak": peak_tf32, "unit": "TFLOP/s", "frac": achieved / peak_tf32,
-                "traffic": traffic,
-                "note": "3xTF32 tensor FLOPs (3 x 2*C*F*tiles*freqs) vs dense TF32 tcgen05 peak, "
-                        + peaks["unit_source"]}
+    if top["name"] == "gemm_output" and engine == "tc":
+        roof = {"bound": "tensor", "kernel": top["name"], "achieved": top["tensor_tflops_3xtf32"],
+                "peak": peaks["tf32_tflops"], "unit": "TFLOP/s", "frac": top["tensor_frac"],
+                "traffic": top["traffic"],
+                "note": "3xTF32 tensor FLOPs per launch (3 x 2*C*F*tiles*freqs) / CUDA-event time vs dense "
+                        "TF32 tcgen05 peak, " + peaks["unit_source"]}
+    elif top["name"] == "conv2d_small_c":
+        roof = {"bound": "fp32", "kernel": top["name"], "achieved": top["fp32_tflops"],
+                "peak": peaks["fp32_tflops"], "unit": "TFLOP/s", "frac": top["fp32_frac"],
+                "traffic": top["traffic"],
+                "note": "C_in<=4: the binding unit is the FP32 pipe (exact reference rounding order on CUDA "
+                        "cores); FP32 lane ops per launch / CUDA-event time vs measured FFMA peak, "
+                        + peaks["unit_source"] + f"; HBM fraction {top['hbm_frac']:.3f}"}
     else:
-        achieved = top["alg_bytes"] / (top["ms"] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": top["name"], "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+        roof = {"bound": "hbm", "kernel": top["name"], "achieved": top["achieved_gbs"], "peak": hbm,
+                "unit": "GB/s", "frac": top["hbm_frac"], "traffic": top["traffic"],
                 "note": "algorithmic bytes per launch / CUDA-event time vs " + peaks["source"]}
-        if top["name"] == "conv2d_small_c":
-            fp = small_c_fp32_ops(desc) / (top["ms"] * 1e-3) / 1e12
-            roof["fp32_pipe"] = {"achieved": fp, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
-                                 "frac": fp / peaks["fp32_tflops"],
-                                 "note": "C_in<=4: the binding unit is the FP32 pipe (exact reference "
-                                         "rounding order on CUDA cores), " + peaks["unit_source"]}
     return roof, kernels
 
 
 def lookup_traffic(workload, kernel, batch):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
-    this kernel from the committed ncu --set full capture, scaled per image to
-    this launch's batch; None when no capture exists for the workload."""
+    this kernel from the committed full-batch ncu --set full capture, scaled
+    per image to this launch's batch; None when no capture exists."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
@@ -488,32 +716,6 @@ def lookup_traffic(workload, kernel, batch):
     if not e:
         return None
     return e["bytes_per_image"] * batch
-
-
-def run_e2e(args, wl, spec, batch, dev, dist, world, dwm_conv2d):
-    """Public-API call with pinned HOST buffers: H2D of x and w, the forward,
-    D2H of y and of the non-finite flag, every step."""
-    import torch
-    xh = torch.randn(batch, wl.c_in, wl.hw, wl.hw).pin_memory()
-    wh = torch.randn(wl.c_out, wl.c_in, wl.kernel, wl.kernel).pin_memory()
-    oh, ow = spec.out_dims(wl.hw, wl.hw)
-    yh = torch.empty(batch, wl.c_out, oh, ow).pin_memory()
-    for _ in range(2):
-        dwm_conv2d(xh, wh, spec, out=yh)
-    torch.cuda.synchronize()
-    steps = max(2, min(args.steps, 5))
-    if dist is not None:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        dwm_conv2d(xh, wh, spec, out=yh)
-    torch.cuda.synchronize()
-    from paper_2002_00552_b200.sharding import max_over_ranks
-    dt = max_over_ranks(time.perf_counter() - t0, dist, dev)
-    return {"value": batch * world * steps / dt, "unit": "images/s",
-            "h2d_bytes_per_step": (xh.numel() + wh.numel()) * 4,
-            "d2h_bytes_per_step": yh.numel() * 4 + 4, "steps": steps,
-            "path": "paper_2002_00552_b200.dwm_conv2d(pinned host tensors, out=pinned host tensor)"}
 
 
 if __name__ == "__main__":

@@ -47,4 +47,4 @@ WORKLOADS = {
     ]
 }
 
-DEFAULT_WORKLOAD = "cfg2-resnet50-stem"
+DEFAULT_WORKLOAD = "cfg4-11x11s1"

@@ -370,7 +370,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
               float* dst = yf + (size_t)(oy + ii) * d.ow + ox;
               if (ox + 1 < d.ow) {
                 bad |= !(isfinite(v[ii][0]) && isfinite(v[ii][1]));
-                if ((d.ow & 1) == 0) {
+                if ((d.ow & 1) == 0 && ((uintptr_t)y & 7) == 0) {
                   __stcs(reinterpret_cast<float2*>(dst), make_float2(v[ii][0], v[ii][1]));
                 } else {
                   __stcs(dst, v[ii][0]);

@@ -314,7 +314,7 @@ small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __r
             float* dst = yf + (size_t)oy * d.ow + ox;
             if (ox + 1 < d.ow) {
               bad |= !(isfinite(v0) && isfinite(v1));
-              if ((d.ow & 1) == 0) {
+              if ((d.ow & 1) == 0 && ((uintptr_t)y & 7) == 0) {
                 __stcs(reinterpret_cast<float2*>(dst), make_float2(v0, v1));
               } else {
                 __stcs(dst, v0);

@@ -267,7 +267,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
   constexpr int VEC = 16 / sizeof(T);
-  if (!WIDE && d.w % VEC == 0) {
+  if (!WIDE && d.w % VEC == 0 && ((uintptr_t)x & 15) == 0) {
     // 16-byte loads over the flattened (channel, row, vector) space, four per
     // thread in flight before the first smem store waits on one
     const int wv = d.w / VEC, nslots = rows_staged * wv, nitems = cb * nslots;

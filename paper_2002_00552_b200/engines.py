@@ -94,9 +94,6 @@ def _check_pair(data, weights):
             f"channel mismatch: data has {data.shape[1]}, weights have {weights.shape[1]}")
 
 
-_WORKSPACE = {}
-
-
 def _zeros_like_io(ref, shape, dt, out=None):
     """Zeros of ``shape`` in the caller's container type (NumPy, or torch on
     the reference tensor's device) -- the result of an empty contraction."""
@@ -110,34 +107,34 @@ def _zeros_like_io(ref, shape, dt, out=None):
     return np.zeros(shape, dtype=dt)
 
 
-def _workspace(device, nbytes: int, stream=None):
-    """Grow-only per-device scratch for V and U (stream-ordered reuse).  When
-    the kernels using it run on a stream other than the allocating (current)
-    one, the buffer is recorded on that stream so torch's caching allocator
-    cannot hand it out again before that stream's work finishes (matters when
-    a later, larger request replaces it)."""
+def _workspace(nbytes: int, device):
+    """Per-call V/U scratch from torch's stream-ordered caching allocator,
+    allocated on the *current* stream (callers run under
+    ``torch.cuda.stream(s)``): a later call on another stream can never be
+    handed this block while this call's kernels still use it, and two calls
+    on two streams never share one."""
     torch = _torch()
-    buf = _WORKSPACE.get(device)
-    if buf is None or buf.numel() < nbytes:
-        _WORKSPACE.pop(device, None)
-        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
-        _WORKSPACE[device] = buf
-    if stream is not None and stream != torch.cuda.current_stream(device):
-        buf.record_stream(stream)
-    return buf
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+
+
+def _aligned(t):
+    """The tensor itself when its base is 16-byte aligned, else an aligned copy
+    (a view with an odd storage offset); the C ABI's workspace-style operands
+    and the kernels' vector paths want 16-byte bases."""
+    return t if t.data_ptr() % 16 == 0 else t.clone()
 
 
 def _batch_chunk(lib, desc, code, algo_code, spec, dev, budget=None) -> int:
     """Largest batch chunk whose workspace fits the device memory budget
-    (free memory plus the cached workspace, with 20 % headroom); the whole
-    batch when it fits."""
+    (free memory plus torch's cached-but-unused blocks, with 20 % headroom);
+    the whole batch when it fits."""
     n = desc.n
     need = lib.dwm_workspace_bytes(desc, code, algo_code)
     if budget is None:
         torch = _torch()
         free, _ = torch.cuda.mem_get_info(dev)
-        cached = _WORKSPACE.get(dev)
-        budget = int(0.8 * (free + (cached.numel() if cached is not None else 0)))
+        cached = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+        budget = int(0.8 * (free + cached))
     if need <= budget or n <= 1:
         return max(n, 1)
     one = lib.dwm_workspace_bytes(_native.make_desc(1, desc.c, desc.h, desc.w, desc.f, spec.kernel,
@@ -145,12 +142,51 @@ def _batch_chunk(lib, desc, code, algo_code, spec, dev, budget=None) -> int:
     return int(max(1, min(n, budget // max(one, 1))))
 
 
-def _check_plan_matches(plan: DecompositionPlan, desc) -> None:
-    rows = [(p.origin, p.step, p.count) for p in plan.row_parts]
-    cols = [(p.origin, p.step, p.count) for p in plan.col_parts]
+def _as_spec(spec) -> ConvSpec:
+    """Accept the reference's own ``ConvSpec`` (or any object with kernel /
+    stride / pad) as well as ours: both normalise to the same int tuples
+    (reference convspec.py:19-28)."""
+    if isinstance(spec, ConvSpec):
+        return spec
+    try:
+        return ConvSpec(kernel=spec.kernel, stride=spec.stride, pad=spec.pad)
+    except AttributeError:
+        raise TypeError(f"spec must be a ConvSpec, got {type(spec).__name__}") from None
+
+
+def _check_plan(plan, spec: ConvSpec) -> None:
+    """reference engines.py:233-236: a caller-supplied plan must be the plan
+    for ``spec``.  Works for the reference's ``DecompositionPlan`` (fields
+    ``spec`` and ``parts`` only, decompose.py:52-57) and ours."""
+    try:
+        pspec = _as_spec(plan.spec)
+    except TypeError:
+        pspec = None
+    if pspec != spec:
+        raise ValueError("plan was built for a different ConvSpec")
+
+
+def _axis_parts_of(plan):
+    """Row and column axis parts of a row-major cross-product plan, derived
+    from ``plan.parts`` (the only part list the reference's plan has)."""
+    parts = [((p.row.origin, p.row.step, p.row.count), (p.col.origin, p.col.step, p.col.count))
+             for p in plan.parts]
+    rows, cols = [], []
+    for r, c in parts:
+        if r not in rows:
+            rows.append(r)
+        if r == parts[0][0]:
+            cols.append(c)
+    if parts != [(r, c) for r in rows for c in cols]:
+        raise ValueError("plan parts are not the row-major cross product of its axis parts")
+    return rows, cols
+
+
+def _check_plan_matches(plan, desc) -> None:
+    rows, cols = _axis_parts_of(plan)
     if rows != desc.axis("row") or cols != desc.axis("col"):
-        raise AssertionError(f"native planner disagrees with the host plan: {rows}/{cols} vs "
-                             f"{desc.axis('row')}/{desc.axis('col')}")
+        raise ValueError(f"plan parts {rows}/{cols} differ from the plan for this ConvSpec "
+                         f"{desc.axis('row')}/{desc.axis('col')}")
 
 
 def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
@@ -166,12 +202,13 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
     CUDA output tensor) and ``stream`` (torch.cuda.Stream; default current).
     """
     _check_pair(data, weights)
+    spec = _as_spec(spec)
     if tuple(weights.shape[2:]) != spec.kernel:
         raise ValueError(f"weights taps {tuple(weights.shape[2:])} do not match kernel {spec.kernel}")
     if plan is None:
         plan = plan_decomposition(spec)
-    elif plan.spec != spec:
-        raise ValueError("plan was built for a different ConvSpec")
+    else:
+        _check_plan(plan, spec)
     dt = _np_dtype(data) if precision is None else precision_dtype(precision)
     n, c, h, w = (int(s) for s in data.shape)
     f = int(weights.shape[0])
@@ -185,61 +222,69 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
 
     torch = _torch()
     lib = _native.load()
+    # host-side planning first (pure C++, no device): the native planner's
+    # axis parts must be the caller's plan
+    desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+    _check_plan_matches(plan, desc)
     if not torch.cuda.is_available():
         raise _native.NativeError("dwm_conv2d needs a CUDA device (B200); there is no CPU fallback")
     tdt = torch.float64 if dt == np.dtype(np.float64) else torch.float32
     code = _native.DWM_F64 if tdt == torch.float64 else _native.DWM_F32
 
-    desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
-    _check_plan_matches(plan, desc)
-
     from_numpy = not _is_torch(data)
     host_in = from_numpy or not data.is_cuda
     dev = (data.device if (not from_numpy and data.is_cuda)
            else torch.device("cuda", torch.cuda.current_device()))
-    w_d = (torch.from_numpy(np.ascontiguousarray(weights)) if not _is_torch(weights)
-           else weights).to(dev, dtype=tdt).contiguous()
     oh, ow = desc.oh, desc.ow
     if out is not None:
-        if tuple(out.shape) != (n, f, oh, ow) or out.dtype != tdt or not out.is_contiguous():
+        if not _is_torch(out) or tuple(out.shape) != (n, f, oh, ow) or out.dtype != tdt \
+                or not out.is_contiguous():
             raise ValueError(f"out must be a contiguous {(n, f, oh, ow)} {tdt} tensor")
+        if host_in and out.is_cuda:
+            raise ValueError("out must be a host tensor when data is on the host")
+        if not host_in and out.device != dev:
+            raise ValueError(f"out must be on {dev} (the device of data), got {out.device}")
     algo_code = _native.ALGOS[algo]
 
     with torch.cuda.device(dev):
         s = stream if stream is not None else torch.cuda.current_stream(dev)
-        flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
-        if host_in:
-            x_h = (torch.from_numpy(np.ascontiguousarray(data)) if from_numpy else data.contiguous())
-            if x_h.dtype != tdt:
-                x_h = x_h.to(tdt)
-            if out is not None and not out.is_cuda:
-                y_h = out
+        # every allocation, conversion, launch and the flag read are ordered
+        # on s (temporaries come from s's pool of the caching allocator)
+        with torch.cuda.stream(s):
+            w_d = _aligned((torch.from_numpy(np.ascontiguousarray(weights)) if not _is_torch(weights)
+                            else weights).to(dev, dtype=tdt).contiguous())
+            flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+            if host_in:
+                x_h = (torch.from_numpy(np.ascontiguousarray(data)) if from_numpy else data.contiguous())
+                if x_h.dtype != tdt:
+                    x_h = x_h.to(tdt)
+                y_h = out if out is not None else torch.empty((n, f, oh, ow), dtype=tdt, pin_memory=True)
+                _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
+                y_res = y_h
             else:
-                y_h = torch.empty((n, f, oh, ow), dtype=tdt, pin_memory=True)
-            _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
-            y_res = y_h
-        else:
-            x_d = data.to(dev, dtype=tdt).contiguous()
-            y_d = out if out is not None else torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
-            # images are independent: when the V workspace of the whole batch
-            # would not fit, run it in batch chunks (same bits per image)
-            chunk = _batch_chunk(lib, desc, code, algo_code, spec, dev)
-            for b0 in range(0, n, chunk):
-                b1 = min(n, b0 + chunk)
-                dk = desc if (b0, b1) == (0, n) else _native.make_desc(
-                    b1 - b0, c, h, w, f, spec.kernel, spec.stride, spec.pad)
-                ws_bytes = lib.dwm_workspace_bytes(dk, code, algo_code)
-                ws = _workspace(dev, ws_bytes, s)
-                st = lib.dwm_conv2d_forward(dk, code, algo_code, x_d[b0].data_ptr(), w_d.data_ptr(),
-                                            y_d[b0].data_ptr(), ws.data_ptr(), ws_bytes,
-                                            flag.data_ptr() if flag is not None else None,
-                                            s.cuda_stream)
-                _native.check(st, "dwm_conv2d_forward")
-            y_res = y_d
-        if counter is not None:
-            counter.elementwise += int(lib.dwm_elementwise_count(desc))
-        if check_finite and int(flag.item()) != 0:
-            raise FloatingPointError("dwm_conv2d produced non-finite values")
+                x_d = data.to(dev, dtype=tdt).contiguous()
+                y_d = out if out is not None else torch.empty((n, f, oh, ow), dtype=tdt, device=dev)
+                # images are independent: when the V workspace of the whole batch
+                # would not fit, run it in batch chunks (same bits per image)
+                chunk = _batch_chunk(lib, desc, code, algo_code, spec, dev)
+                for b0 in range(0, n, chunk):
+                    b1 = min(n, b0 + chunk)
+                    dk = desc if (b0, b1) == (0, n) else _native.make_desc(
+                        b1 - b0, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+                    ws_bytes = lib.dwm_workspace_bytes(dk, code, algo_code)
+                    ws = _workspace(ws_bytes, dev)
+                    st = lib.dwm_conv2d_forward(dk, code, algo_code, x_d[b0].data_ptr(), w_d.data_ptr(),
+                                                y_d[b0].data_ptr(), ws.data_ptr(), ws_bytes,
+                                                flag.data_ptr() if flag is not None else None,
+                                                s.cuda_stream)
+                    _native.check(st, "dwm_conv2d_forward")
+                    del ws
+                y_res = y_d
+            if counter is not None:
+                counter.elementwise += int(lib.dwm_elementwise_count(desc))
+            # .item() copies on s and waits for it
+            if check_finite and int(flag.item()) != 0:
+                raise FloatingPointError("dwm_conv2d produced non-finite values")
     if from_numpy:
         return y_res.numpy()
     return y_res
@@ -259,7 +304,7 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
     """Host-resident input/output: the batch is cut into chunks whose
     host->device copy, forward and device->host copy run on three streams, so
     PCIe traffic in both directions overlaps the kernels (images are
-    independent, so chunking changes no result bit)."""
+    independent, so chunking changes no result bit).  Runs with ``s`` current."""
     torch = _torch()
     n = x_h.shape[0]
     chunks = 1 if n < 2 else min(8, n)
@@ -268,10 +313,11 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
     y_d = torch.empty(y_h.shape, dtype=y_h.dtype, device=dev)
     s_in, s_out = _side_streams(dev)
     s_in.wait_stream(s)
+    s_out.wait_stream(s)
     ws_bytes = max(lib.dwm_workspace_bytes(_native.make_desc(
         b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad), code, algo_code)
         for b0, b1 in zip(bounds, bounds[1:]))
-    ws = _workspace(dev, ws_bytes, s)
+    ws = _workspace(ws_bytes, dev)
     for b0, b1 in zip(bounds, bounds[1:]):
         with torch.cuda.stream(s_in):
             x_d[b0:b1].copy_(x_h[b0:b1], non_blocking=True)
@@ -279,6 +325,8 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
             ev_in.record(s_in)
         s.wait_event(ev_in)
         dk = _native.make_desc(b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad)
+        # chunk bases need only natural alignment (the kernels take their
+        # vector paths only on 16-/8-byte aligned bases)
         st = lib.dwm_conv2d_forward(dk, code, algo_code, x_d[b0].data_ptr(), w_d.data_ptr(),
                                     y_d[b0].data_ptr(), ws.data_ptr(), ws_bytes,
                                     flag.data_ptr() if flag is not None else None, s.cuda_stream)
@@ -288,8 +336,8 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
         s_out.wait_event(ev_done)
         with torch.cuda.stream(s_out):
             y_h[b0:b1].copy_(y_d[b0:b1], non_blocking=True)
-    # device buffers are freed to torch's caching allocator only after the
-    # side streams are done with them
+    # device buffers go back to the caching allocator only after the side
+    # streams are done with them
     x_d.record_stream(s_in)
     y_d.record_stream(s_out)
     s.wait_stream(s_out)
@@ -380,7 +428,7 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
     """
     _check_pair(data, weights)
     _require_tensor4(grad_out, "grad_out")
-    spec = plan.spec
+    spec = _as_spec(plan.spec)
     if tuple(weights.shape[2:]) != spec.kernel:
         raise ValueError(f"weights taps {tuple(weights.shape[2:])} do not match kernel {spec.kernel}")
     n, c, h, w = (int(s) for s in data.shape)
@@ -418,7 +466,7 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
                 desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
                 wg_algo = _native.ALGOS[wgrad_algo]
                 wg_bytes = int(lib.dwm_weight_grad_workspace_bytes(desc, code, wg_algo))
-                wg_ws = _workspace(dev, wg_bytes)
+                wg_ws = _workspace(wg_bytes, dev)
                 _native.check(lib.dwm_weight_grad(desc, code, wg_algo, x.data_ptr(), dy.data_ptr(),
                                                   gw.data_ptr(), wg_ws.data_ptr(), wg_bytes, s.cuda_stream),
                               "dwm_weight_grad")
@@ -451,4 +499,4 @@ def flops_dwm(plan: DecompositionPlan, out) -> int:
     the transform terms are zero because F(2,<=3) is shift-free)."""
     oh, ow = out
     tiles = -(-oh // 2) * -(-ow // 2)
-    return tiles * plan.num_frequencies
+    return tiles * sum((p.row.count + 1) * (p.col.count + 1) for p in plan.parts)

@@ -20,17 +20,26 @@ This module is that operator on B200:
 CUDA tensors only: there is no CPU fallback.
 """
 
+import weakref
+
 import numpy as np
 import torch
 
 from . import _native
 from .convspec import ConvSpec
 from .decompose import DecompositionPlan, plan_decomposition
-from .engines import _workspace, dwm_backward
+from .engines import _aligned, _as_spec, _check_plan, _workspace, dwm_backward
 
 
 class FilterCache:
-    """Transformed-filter cache, one entry per weight tensor identity."""
+    """Transformed-filter cache, one entry per live weight tensor.
+
+    An entry holds a weak reference to the caller's weight tensor and the
+    ``_version`` it was transformed at; a hit needs the very same tensor
+    object (not merely the same address: the caching allocator reuses
+    addresses, and a fresh tensor starts at version 0) at the same version.
+    Non-contiguous and inference tensors are never cached (their contiguous
+    copy is a new object per call; an inference tensor has no version)."""
 
     def __init__(self, capacity: int = 64):
         self.capacity = capacity
@@ -43,25 +52,35 @@ class FilterCache:
 
     @staticmethod
     def transform(lib, desc, code: int, algo_code: int, w: torch.Tensor, stream) -> torch.Tensor:
+        w = w.contiguous()
         u = torch.empty(max(int(lib.dwm_filter_bytes(desc, code, algo_code)), 1), dtype=torch.uint8,
                         device=w.device)
         _native.check(lib.dwm_prepare_filter(desc, code, algo_code, w.data_ptr(), u.data_ptr(),
                                              stream.cuda_stream), "dwm_prepare_filter")
         return u
 
+    @staticmethod
+    def cacheable(w: torch.Tensor) -> bool:
+        return w.is_contiguous() and not w.is_inference() and w.data_ptr() % 16 == 0
+
     def get(self, lib, desc, code: int, algo_code: int, w: torch.Tensor, stream) -> torch.Tensor:
+        """U for the caller's weight tensor ``w`` (before any .contiguous())."""
+        if not self.cacheable(w):
+            self.misses += 1
+            return self.transform(lib, desc, code, algo_code, w, stream)
         tc = lib.dwm_select_algo(desc, code, algo_code) == _native.ALGOS["tc"]
         key = (w.data_ptr(), w.device, w.dtype, tc, desc.f, desc.c, desc.r_h, desc.r_w,
                desc.s_h, desc.s_w)
         hit = self._entries.get(key)
-        if hit is not None and hit[0] == w._version:
+        if hit is not None and hit[0]() is w and hit[1] == w._version:
             self.hits += 1
-            return hit[1]
+            return hit[2]
         self.misses += 1
         u = self.transform(lib, desc, code, algo_code, w, stream)
+        self._entries.pop(key, None)
         if len(self._entries) >= self.capacity:
             self._entries.pop(next(iter(self._entries)))
-        self._entries[key] = (w._version, u)
+        self._entries[key] = (weakref.ref(w), w._version, u)
         return u
 
 
@@ -88,17 +107,16 @@ def _forward(x: torch.Tensor, w: torch.Tensor, spec: ConvSpec, algo: str, cache:
     algo_code = _native.ALGOS[algo]
     n, c, h, wd = (int(v) for v in x.shape)
     desc = _native.make_desc(n, c, h, wd, int(w.shape[0]), spec.kernel, spec.stride, spec.pad)
-    x = x.contiguous()
-    w = w.contiguous()
+    x = _aligned(x.contiguous())
     with torch.cuda.device(x.device):
         s = torch.cuda.current_stream(x.device)
         if cache is None:
-            u = FilterCache.transform(lib, desc, code, algo_code, w, s)
+            u = FilterCache.transform(lib, desc, code, algo_code, _aligned(w.contiguous()), s)
         else:
             u = cache.get(lib, desc, code, algo_code, w, s)
         y = torch.empty((n, desc.f, desc.oh, desc.ow), dtype=x.dtype, device=x.device)
         ws_bytes = int(lib.dwm_workspace_bytes(desc, code, algo_code))
-        ws = _workspace(x.device, ws_bytes)
+        ws = _workspace(ws_bytes, x.device)
         flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
         _native.check(lib.dwm_conv2d_forward_prepared(
             desc, code, algo_code, x.data_ptr(), u.data_ptr(), y.data_ptr(), ws.data_ptr(), ws_bytes,
@@ -135,10 +153,11 @@ class DWMConv2dFunction(torch.autograd.Function):
 def dwm_conv2d_op(x: torch.Tensor, w: torch.Tensor, spec: ConvSpec, plan: DecompositionPlan = None,
                   algo: str = "auto", cache: FilterCache = None, check_finite: bool = True):
     """Functional, differentiable DWM convolution of CUDA tensors."""
+    spec = _as_spec(spec)
     if plan is None:
         plan = plan_decomposition(spec)
-    elif plan.spec != spec:
-        raise ValueError("plan was built for a different ConvSpec")
+    else:
+        _check_plan(plan, spec)
     return DWMConv2dFunction.apply(x, w, spec, plan, algo, _cache_for(w, cache or DEFAULT_CACHE),
                                    check_finite)
 

@@ -15,6 +15,9 @@ import pytest
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 REF_SRC = Path("/root/reference/pkg/src")
+# the unmodified reference installed by bench.py's reference arm recipe
+# (pip install --target baseline/_ref); travels to the GPU box
+REF_INSTALLED = ROOT / "baseline" / "_ref"
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
@@ -22,15 +25,23 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
 
 
+def _reference_dir():
+    for d in (REF_SRC, REF_INSTALLED):
+        if (d / "dwmconv" / "__init__.py").exists():
+            return d
+    return None
+
+
 def reference_available() -> bool:
-    return (REF_SRC / "dwmconv" / "__init__.py").exists()
+    return _reference_dir() is not None
 
 
 def import_reference():
-    if not reference_available():
-        pytest.skip("reference package not present (GPU box); golden fixtures cover this")
-    if str(REF_SRC) not in sys.path:
-        sys.path.append(str(REF_SRC))
+    d = _reference_dir()
+    if d is None:
+        pytest.skip("reference package not present; golden fixtures cover this")
+    if str(d) not in sys.path:
+        sys.path.append(str(d))
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
     sys.dont_write_bytecode = True
     import dwmconv

@@ -19,6 +19,9 @@ and writes:
   backward_cases.json on the reference's backward test geometries plus
                       asymmetric/rectangular/channel-heavy extras
                       (``make_golden.py backward`` regenerates only these)
+  accuracy_14x14.json the reference's binary32 acceptance sweep (C=F=256,
+                      14x14, r=3..11, seeds 1-3): DWM32 / direct32 MSE
+                      (``make_golden.py acceptance`` regenerates only this)
 The GPU box has no /root/reference; the tests there read these files.
 """
 
@@ -145,6 +148,29 @@ def baseline_samples():
     (HERE / "baseline_samples.json").write_text(json.dumps(out))
 
 
+def acceptance_14x14():
+    """The reference's own binary32 acceptance sweep (data/accuracy_14x14.json:
+    C=F=256, 14x14, r=3..11 stride 1, seeds 1-3; test_acceptance.py:137-168),
+    run through the reference's accuracy harness (bench.run_accuracy_suite):
+    DWM32 and direct32 MSE vs the binary64 direct conv per (r, seed)."""
+    from dwmconv.bench import AccuracyConfig, run_accuracy_suite
+    spec = json.loads(Path("/root/reference/pkg/src/dwmconv/data/accuracy_14x14.json").read_text())
+    rows = []
+    for c in spec["configs"]:
+        cfg = AccuracyConfig(kernel=(c["kernel"],) * 2, stride=(c["stride"],) * 2, hw=c["hw"],
+                             channels=c["channels"], filters=c["filters"], batch=c["batch"],
+                             precisions=("binary32",))
+        rep = run_accuracy_suite([cfg], seeds=spec["seeds"])
+        for r in rep.rows:
+            if r.precision == "binary32" and r.algorithm in ("dwm", "direct"):
+                rows.append({"kernel": c["kernel"], "stride": c["stride"], "hw": c["hw"],
+                             "channels": c["channels"], "filters": c["filters"], "batch": c["batch"],
+                             "seed": r.seed, "algorithm": r.algorithm, "mse": r.mse})
+        print(f"r={c['kernel']}: " + ", ".join(f"{x['algorithm']} s{x['seed']} {x['mse']:.3e}"
+                                             for x in rows if x["kernel"] == c["kernel"]), flush=True)
+    (HERE / "accuracy_14x14.json").write_text(json.dumps({"seeds": spec["seeds"], "rows": rows}, indent=1))
+
+
 def backward_case_specs():
     cases = []
     # test_engines_backward.py:81-98 (+ the finite-difference and degenerate cases)
@@ -206,7 +232,11 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["backward"]:
         backward_cases()
         sys.exit(0)
+    if sys.argv[1:] == ["acceptance"]:
+        acceptance_14x14()
+        sys.exit(0)
     backward_cases()
+    acceptance_14x14()
     plans()
     transforms()
     small_cases()

@@ -73,3 +73,46 @@ def test_empty_tensors_match_live_reference(ref):
     want = ref.dwm_conv2d(d, g, ref.ConvSpec(kernel=(3, 3)))
     got = dwm_conv2d(d, g, ConvSpec(kernel=(3, 3)))
     assert got.shape == want.shape and got.dtype == want.dtype and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kernel,stride,pad", [((7, 7), (2, 2), (3, 3, 3, 3)), ((11, 5), (4, 1), (0, 1, 2, 0)),
+                                               ((3, 3), (1, 1), (1, 1, 1, 1))])
+def test_reference_spec_and_plan_objects_reach_native_planner(ref, monkeypatch, kernel, stride, pad):
+    """Drop-in with the reference's own objects (engines.py:233-236,417-418):
+    its ConvSpec and DecompositionPlan (fields spec/parts only) pass the plan
+    check and reach dwm_desc_init; the first thing that fails on this CPU-only
+    host is the device check, after all host-side planning."""
+    import torch
+    from paper_2002_00552_b200 import engines, flops_dwm
+    seen = {}
+    real = engines._check_plan_matches
+
+    def spy(plan, desc):
+        real(plan, desc)
+        seen["rows"], seen["cols"] = desc.axis("row"), desc.axis("col")
+    monkeypatch.setattr(engines, "_check_plan_matches", spy)
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    rspec = ref.ConvSpec(kernel=kernel, stride=stride, pad=pad)
+    rplan = ref.plan_decomposition(rspec)
+    d = np.zeros((1, 2, 23, 19), np.float32)
+    g = np.zeros((3, 2, *kernel), np.float32)
+    for sp, pl in ((rspec, rplan), (rspec, None), (ConvSpec(kernel=kernel, stride=stride, pad=pad), rplan)):
+        seen.clear()
+        with pytest.raises(RuntimeError, match="no CPU fallback"):
+            dwm_conv2d(d, g, sp, plan=pl)
+        want_rows = []
+        for p in rplan.parts:
+            r = (p.row.origin, p.row.step, p.row.count)
+            if r not in want_rows:
+                want_rows.append(r)
+        assert seen["rows"] == want_rows
+    # the reference's FlopCounter and plan work with the counting helpers
+    oh, ow = rspec.out_dims(23, 19)
+    assert flops_dwm(rplan, (oh, ow)) == ref.flops_dwm(rplan, (oh, ow))
+
+
+def test_reference_plan_for_other_spec_is_rejected(ref):
+    rspec = ref.ConvSpec(kernel=(5, 5), stride=(1, 1), pad=(2, 2, 2, 2))
+    other = ref.plan_decomposition(ref.ConvSpec(kernel=(5, 5), stride=(2, 2), pad=(2, 2, 2, 2)))
+    with pytest.raises(ValueError, match="different ConvSpec"):
+        dwm_conv2d(np.zeros((1, 1, 8, 8)), np.zeros((1, 1, 5, 5)), rspec, plan=other)

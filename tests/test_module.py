@@ -125,3 +125,55 @@ def test_training_matches_nn_conv2d(cuda):
     assert (m.bias - ref.bias).abs().max().item() <= 1e-10
     with torch.no_grad():
         assert (m(x) - ref(x)).abs().max().item() <= 1e-10
+
+
+class _FakeLib:
+    """Host stand-in for the native library: FilterCache.get only asks it for
+    the engine selection; the transform itself is stubbed."""
+
+    def dwm_select_algo(self, desc, code, algo):
+        return 2
+
+
+def _desc():
+    from types import SimpleNamespace
+    return SimpleNamespace(f=4, c=3, r_h=3, r_w=3, s_h=1, s_w=1)
+
+
+def test_filter_cache_identity_version_and_uncacheable(monkeypatch):
+    """The cache hits only for the same live tensor object at the same
+    version: a new tensor at a recycled address, an in-place update, a
+    non-contiguous weight and an inference tensor all re-transform."""
+    import torch
+    from paper_2002_00552_b200.module import FilterCache
+    calls = []
+
+    def fake_transform(lib, desc, code, algo_code, w, stream):
+        calls.append(w.data_ptr())
+        return torch.tensor([float(len(calls))])
+    monkeypatch.setattr(FilterCache, "transform", staticmethod(fake_transform))
+    cache, lib, d = FilterCache(), _FakeLib(), _desc()
+    w = torch.randn(4, 3, 3, 3)
+    u1 = cache.get(lib, d, 0, 0, w, None)
+    assert cache.get(lib, d, 0, 0, w, None) is u1 and len(calls) == 1        # same tensor, same version
+    with torch.no_grad():
+        w.add_(1.0)                                                          # optimizer-style update
+    assert cache.get(lib, d, 0, 0, w, None) is not u1 and len(calls) == 2
+    # a new tensor at (possibly) the same address starts at _version 0: must miss
+    ptr = w.data_ptr()
+    del w
+    w2 = torch.empty(4, 3, 3, 3).normal_()
+    n0 = len(calls)
+    cache.get(lib, d, 0, 0, w2, None)
+    assert len(calls) == n0 + 1, f"stale hit (same address reused: {w2.data_ptr() == ptr})"
+    # non-contiguous (channels_last) weights: never cached, always re-transformed
+    wc = torch.randn(4, 3, 3, 3).to(memory_format=torch.channels_last)
+    assert not wc.is_contiguous()
+    cache.get(lib, d, 0, 0, wc, None)
+    cache.get(lib, d, 0, 0, wc, None)
+    assert len(calls) == n0 + 3
+    # inference tensors have no version counter: bypass, no error
+    with torch.inference_mode():
+        wi = torch.randn(4, 3, 3, 3)
+    cache.get(lib, d, 0, 0, wi, None)
+    assert len(calls) == n0 + 4

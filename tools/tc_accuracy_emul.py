@@ -15,6 +15,9 @@ Schemes:
   split<K>  main (hi*hi) accumulator per K channels, one correction
             accumulator over all channels; mq = sum(main chunks) + corr
   long      one accumulator over all channels (corr first per 32 ch)
+  pair<S>   main (hi*hi) and correction (hi*lo + lo*hi) in two accumulators,
+            both fresh per S channels (one N=128 MMA [Uh;Ul] + one N=64
+            MMA Vl*Uh per K step); chunk = main + corr, chunks summed in FP32
 
     python tools/tc_accuracy_emul.py [--workloads cfg4-7x7s1,...] [--filters 64]
 """
@@ -89,6 +92,19 @@ def contraction(V, U, scheme):
             for k in kk:
                 acc = step(acc, vh[..., k], uh[..., k], False)
             mq = acc if mq is None else (mq + acc).astype(np.float32)
+        return mq
+    if scheme.startswith("pair"):
+        span = int(scheme[len("pair"):])
+        mq = None
+        for c0 in range(0, C, span):
+            kk = ks[c0 // 8:(c0 + span) // 8]
+            acc = corr = None
+            for i, k in enumerate(kk):
+                acc = step(acc, vh[..., k], uh[..., k], i == 0)
+                corr = step(corr, vh[..., k], ul[..., k], i == 0)
+                corr = step(corr, vl[..., k], uh[..., k], False)
+            chunk = (acc + corr).astype(np.float32)
+            mq = chunk if mq is None else (mq + chunk).astype(np.float32)
         return mq
     kch = int(scheme[len("split"):])
     corr = None
