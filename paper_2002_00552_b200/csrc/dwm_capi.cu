@@ -6,6 +6,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "dwm_common.cuh"
 #include "dwm_kernels.h"
@@ -25,6 +28,50 @@ int fail(int status, const char* fmt, ...) {
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   return fail(DWM_ECUDA, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
               cudaGetErrorString(e), what, file, line);
+}
+
+namespace {
+std::mutex g_launch_mu;
+std::map<std::pair<const void*, int>, size_t> g_smem_set;           // (kernel, device) -> bytes set
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occupancy;  // (kernel, device, threads, smem)
+int g_sms[64];
+}  // namespace
+
+int device_sm_count(int* sms) {
+  int dev = 0;
+  DWM_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  int& v = g_sms[dev & 63];
+  if (!v) DWM_CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  *sms = v;
+  return DWM_OK;
+}
+
+int ensure_dynamic_smem(const void* kernel, size_t smem) {
+  int dev = 0;
+  DWM_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  size_t& have = g_smem_set[{kernel, dev}];
+  if (smem > have || have == 0) {
+    DWM_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    have = smem > have ? smem : have;
+  }
+  return DWM_OK;
+}
+
+int cached_occupancy(const void* kernel, int threads, size_t smem, int* per_sm) {
+  int dev = 0;
+  DWM_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  auto key = std::make_tuple(kernel, dev, threads, smem);
+  auto it = g_occupancy.find(key);
+  if (it == g_occupancy.end()) {
+    int v = 0;
+    DWM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, smem));
+    it = g_occupancy.emplace(key, v).first;
+  }
+  *per_sm = it->second;
+  return DWM_OK;
 }
 
 // decompose.py:73-100 -- stride split, then size split of each residue run.
@@ -132,7 +179,7 @@ size_t dwm_workspace_bytes(const dwm_desc_t* d, int dtype, int algo) {
   const size_t es = dtype == DWM_F64 ? 8 : 4;
   const int sel = dwm_select_algo(d, dtype, algo);
   size_t u = (size_t)d->num_freqs * (size_t)d->f * (size_t)d->c * es;
-  if (sel == DWM_ALGO_TC) u *= 2;  // hi/lo TF32 split of U
+  if (sel == DWM_ALGO_TC) u = tc_filter_bytes(*d);  // stacked hi/lo TF32 split of U
   const size_t v = sel == DWM_ALGO_SMALL_C ? 0 : v_bytes_of(d, es);
   return round_up(v, 256) + round_up(u, 256);
 }
@@ -239,7 +286,7 @@ size_t dwm_filter_bytes(const dwm_desc_t* d, int dtype, int algo) {
   if (!d) return 0;
   const size_t es = dtype == DWM_F64 ? 8 : 4;
   size_t u = (size_t)d->num_freqs * (size_t)d->f * (size_t)d->c * es;
-  if (dwm_select_algo(d, dtype, algo) == DWM_ALGO_TC) u *= 2;
+  if (dwm_select_algo(d, dtype, algo) == DWM_ALGO_TC) u = tc_filter_bytes(*d);
   return u;
 }
 

@@ -61,6 +61,13 @@ __host__ __device__ __forceinline__ int part_freq_offset(const dwm_desc_t& d, in
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 int fail(int status, const char* fmt, ...);
 
+// Host-side launch facts cached per (kernel, device) instead of queried on
+// every launch (dwm_capi.cu): SM count, the dynamic-smem attribute (set only
+// when a kernel needs more than it was last given) and CTAs per SM.
+int device_sm_count(int* sms);
+int ensure_dynamic_smem(const void* kernel, size_t smem);
+int cached_occupancy(const void* kernel, int threads, size_t smem, int* per_sm);
+
 // ---- packed f32x2 (FFMA2 / FADD2 / FMUL2: two lanes of work per issue slot) ----
 typedef unsigned long long f2;
 __device__ __forceinline__ f2 pk(float a, float b) {

@@ -7,7 +7,9 @@
 namespace dwm {
 
 int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s);
-// U_hi | U_lo (each [freq][F][C] fp32, TF32-valued, RN split) for the tcgen05 path.
+// U for the tcgen05 path: TF32-valued RN split U_hi / U_lo, stacked per
+// 64-filter block: [freq][ceil(F/64)][U_hi 64 rows; U_lo 64 rows][C] (zero rows
+// past F), so one TMA box gives the GEMM its [U_hi; U_lo] N = 128 B operand.
 int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s);
 int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s);
 int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void* U, void* y,
@@ -23,6 +25,7 @@ bool small_c_supported(const dwm_desc_t& d);
 int launch_small_c(const dwm_desc_t& d, const void* x, const void* U, void* y, int32_t* flag,
                    cudaStream_t s);
 bool tc_gemm_supported(const dwm_desc_t& d);
+size_t tc_filter_bytes(const dwm_desc_t& d);
 int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag,
                    cudaStream_t s);
 

@@ -83,6 +83,14 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* desc, ui
       : "memory");
 }
 
+// L2 prefetch of a 3-D tile (no smem, no completion): hides the DRAM latency
+// of a later tma_load_3d of the same box.
+__device__ __forceinline__ void tma_prefetch_3d(const void* desc, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(desc), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
+}
+
 // One lane of a converged warp (elect.sync).  Issuing tcgen05/TMA from a
 // converged warp lets ptxas keep the operands in uniform registers; issuing
 // from a lane-divergent branch costs an R2UR/ELECT loop per instruction and
@@ -151,6 +159,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
       : "r"(taddr));
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 32 lanes x 8 consecutive 32-bit columns per warp.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 // 32 lanes x 32 consecutive 32-bit columns per warp.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {

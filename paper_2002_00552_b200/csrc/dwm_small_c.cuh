@@ -335,11 +335,11 @@ small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __r
 template <class K>
 int launch_cfg(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
   const size_t smem = K::smem_bytes(d.num_freqs);
-  DWM_CUDA_TRY(cudaFuncSetAttribute(small_c_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 0, per_sm = 0;
-  DWM_CUDA_TRY(cudaGetDevice(&dev));
-  DWM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DWM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_c_kernel<K>, THREADS, smem));
+  const void* kern = (const void*)small_c_kernel<K>;
+  if (int st = ensure_dynamic_smem(kern, smem)) return st;
+  int sms = 0, per_sm = 0;
+  if (int st = device_sm_count(&sms)) return st;
+  if (int st = cached_occupancy(kern, THREADS, smem, &per_sm)) return st;
   if (per_sm < 1) return fail(DWM_EUNSUPPORTED, "small-C kernel does not fit (smem %zu B)", smem);
   const int fblocks = (d.f + K::BN - 1) / K::BN;
   const int64_t nblocks = (d.tiles + K::BM - 1) / K::BM;

@@ -83,14 +83,19 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
-// U_hi = tf32(U), U_lo = tf32(U - U_hi), two [freq][F][C] planes.
+// U_hi = tf32(U), U_lo = tf32(U - U_hi), stacked per 64-filter block:
+// U[((fq * nblk + f / 64) * 128 + {0: hi, 64: lo} + f % 64) * C + c]; one
+// thread per (f, c) over the padded filter count (rows past F are zeros).
 __global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const float* __restrict__ w,
                                                   float* __restrict__ U) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t fc = (int64_t)d.f * d.c;
-  if (idx >= fc) return;
-  const int64_t plane = (int64_t)d.num_freqs * fc;
-  const float* wfc = w + idx * d.r_h * d.r_w;
+  const int nblk = (d.f + 63) / 64;
+  const int64_t fcp = (int64_t)nblk * 64 * d.c;
+  if (idx >= fcp) return;
+  const int f = (int)(idx / d.c), c = (int)(idx % d.c);
+  const bool live = f < d.f;
+  const float* wfc = w + (live ? (int64_t)f * d.c + c : 0) * d.r_h * d.r_w;
+  const int64_t row0 = (int64_t)(f / 64) * 128 + f % 64;
   int fq = 0;
   for (int rp = 0; rp < d.n_row_parts; ++rp)
     for (int cp = 0; cp < d.n_col_parts; ++cp) {
@@ -102,11 +107,12 @@ __global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const floa
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           if (a < lr && b < lc) {
-            const float hi = tf32_rn(u[a][b]);
-            const float lo = tf32_rn(u[a][b] - hi);
-            const int64_t o = (int64_t)(fq + a * lc + b) * fc + idx;
+            const float v = live ? u[a][b] : 0.f;
+            const float hi = tf32_rn(v);
+            const float lo = tf32_rn(v - hi);
+            const int64_t o = ((int64_t)(fq + a * lc + b) * nblk * 128 + row0) * d.c + c;
             U[o] = hi;
-            U[plane + o] = lo;
+            U[o + 64 * (int64_t)d.c] = lo;
           }
       fq += lr * lc;
     }
@@ -394,7 +400,7 @@ int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void*
 }
 
 int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s) {
-  const int64_t n = (int64_t)d.f * d.c;
+  const int64_t n = (int64_t)((d.f + 63) / 64) * 64 * d.c;
   filter_transform_tf32split_kernel<<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, (float*)U);
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
@@ -447,7 +453,7 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   const bool stream = d.num_freqs > IT_STREAM_MIN_FREQS;
   auto kern = wide ? (stream ? input_transform_smem_kernel<T, true, true> : input_transform_smem_kernel<T, true, false>)
                    : (stream ? input_transform_smem_kernel<T, false, true> : input_transform_smem_kernel<T, false, false>);
-  DWM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int st = ensure_dynamic_smem((const void*)kern, smem)) return st;
   // warps: a divisor of the tile count in [4, 8] so every warp gets the same number of tiles
   int warps = 8;
   if (twb <= 8) warps = twb;

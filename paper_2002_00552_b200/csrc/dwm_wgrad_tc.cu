@@ -368,10 +368,9 @@ int launch_wgrad_tc(const dwm_desc_t& d, const void* x, const void* dy, void* gw
     if (int st = encode(&ml, dlo, 2, dims, strides, box)) return st;
   }
   const size_t smem = sizeof(WSmem) + 1024;
-  DWM_CUDA_TRY(cudaFuncSetAttribute(wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 0;
-  DWM_CUDA_TRY(cudaGetDevice(&dev));
-  DWM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (int st = ensure_dynamic_smem((const void*)wgrad_tc_kernel, smem)) return st;
+  int sms = 0;
+  if (int st = device_sm_count(&sms)) return st;
   const int64_t items = (int64_t)d.num_freqs * ((d.c + BM - 1) / BM) * ((d.f + BN - 1) / BN);
   const int grid = (int)(items < sms ? items : sms);
   wgrad_tc_kernel<<<grid, THREADS, smem, s>>>(d, tp, mv, mh, ml, du);

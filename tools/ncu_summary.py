@@ -14,9 +14,13 @@ keys = ["gpu__time_duration.sum", "launch__registers_per_thread", "sm__warps_act
         "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
-        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_sectors_srcunit_tex.sum",
+        "lts__t_sectors_srcunit_tex.sum.pct_of_peak_sustained_elapsed", "lts__t_sectors_srcunit_ltcfabric.sum.pct_of_peak_sustained_elapsed",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size"]
+units = dict(zip(hdr, rows[1]))
 for k in keys:
-    if k in d: print(f"{k:80s} {d[k]}")
+    if k in d: print(f"{k:80s} {d[k]} {units.get(k, '')}")
 st = [(h.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(v.replace(",", "") or 0)) for h, v in d.items()
       if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")]
 tot = sum(v for _, v in st) or 1
