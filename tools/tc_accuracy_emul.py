@@ -93,6 +93,26 @@ def contraction(V, U, scheme):
                 acc = step(acc, vh[..., k], uh[..., k], False)
             mq = acc if mq is None else (mq + acc).astype(np.float32)
         return mq
+    if scheme.startswith("pairc"):
+        # pair<S> plus a truncation-bias compensation: each of the S/8 main
+        # steps truncates toward zero by ~0.5 ulp on average, so add back
+        # alpha * steps * ulp(main) in the direction of main (scheme pairc<S>_<alpha*100>)
+        span, alpha = scheme[len("pairc"):].split("_")
+        span, alpha = int(span), int(alpha) / 100.0
+        mq = None
+        for c0 in range(0, C, span):
+            kk = ks[c0 // 8:(c0 + span) // 8]
+            acc = corr = None
+            for i, k in enumerate(kk):
+                acc = step(acc, vh[..., k], uh[..., k], i == 0)
+                corr = step(corr, vh[..., k], ul[..., k], i == 0)
+                corr = step(corr, vl[..., k], uh[..., k], False)
+            e = np.floor(np.log2(np.maximum(np.abs(acc.astype(np.float64)), 1e-38)))
+            ulp = np.exp2(e - 23).astype(np.float32)
+            comp = (np.sign(acc) * np.float32(alpha * len(kk)) * ulp).astype(np.float32)
+            chunk = ((acc + comp).astype(np.float32) + corr).astype(np.float32)
+            mq = chunk if mq is None else (mq + chunk).astype(np.float32)
+        return mq
     if scheme.startswith("pair"):
         span = int(scheme[len("pair"):])
         mq = None
