@@ -115,13 +115,31 @@ __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.
 template <uint32_t N>
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
+// The tcgen05 FP32 accumulator truncates each K = 8 step toward zero (about
+// -0.5 ulp per step, tools/tc_accum_probe.cu), so a chunk of n main-product
+// steps is biased toward zero by ~n/2 ulp of its value.  For the 32-channel
+// chunks (4 steps, C < 128, where the GEMM error weighs most) the epilogue
+// adds back 1 ulp away from zero -- one integer add on the float's bits (a
+// mantissa carry into the exponent is still +1 ulp) -- emulated MSE 0.56-0.70x
+// the reference DWM32's instead of 0.70-0.86x (tools/tc_accuracy_emul.py
+// "pairc32_25").  The 64-channel chunks do not use it: on the C >= 128
+// shapes the extra epilogue latency cost 4-8 % (profiles/r2/ab_tc_bias_comp_chunk128.txt)
+// and their MSE is already 0.2-0.55x.
+__device__ __forceinline__ float trunc_compensate(float x, uint32_t k) {
+  return __uint_as_float(__float_as_uint(x) + k);
+}
+
 // Stage geometry: stage kc of a frequency covers channels [64 kc, 64 kc + 64);
 // a C % 64 == 32 tail stage has one atom (4 K-slices).
 __device__ __forceinline__ int stage_atoms(int C, int kc) { return C - SK * kc >= SK ? 2 : 1; }
 
+// C32: 32-channel accumulator chunks (C < 128) with the truncation-bias
+// compensation; otherwise 64-channel chunks, uncompensated.
+template <bool C32>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_u,
-               float* __restrict__ y, int32_t* __restrict__ flag, int chunk32) {
+               float* __restrict__ y, int32_t* __restrict__ flag) {
+  constexpr bool chunk32 = C32;
   extern __shared__ uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -334,7 +352,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
               tmem_ld_wait();
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float part = __fadd_rn(mn[j], cr[j]);
+                const float part = __fadd_rn(chunk32 ? trunc_compensate(mn[j], 1u) : mn[j], cr[j]);
                 mq[8 * h + j] = first ? part : __fadd_rn(mq[8 * h + j], part);
               }
             }
@@ -485,10 +503,15 @@ int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, i
   const size_t smem = sizeof(Smem) + 1024;
   int sms = 0;
   if (int st = device_sm_count(&sms)) return st;
-  if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel, smem)) return st;
   const int64_t items = ((d.tiles + BM - 1) / BM) * ((d.f + BN - 1) / BN);
   const int grid = (int)(items < sms ? items : sms);
-  gemm_tc_kernel<<<grid, THREADS, smem, s>>>(d, mv, mu, (float*)y, flag, tc_chunk32(d));
+  if (tc_chunk32(d)) {
+    if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<true>, smem)) return st;
+    gemm_tc_kernel<true><<<grid, THREADS, smem, s>>>(d, mv, mu, (float*)y, flag);
+  } else {
+    if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<false>, smem)) return st;
+    gemm_tc_kernel<false><<<grid, THREADS, smem, s>>>(d, mv, mu, (float*)y, flag);
+  }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }

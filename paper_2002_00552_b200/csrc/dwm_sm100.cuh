@@ -51,15 +51,24 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 // Spin on an mbarrier phase.  A wait that exceeds ~2 s means a protocol bug
-// (a TMA or MMA that never completes): trap instead of hanging the GPU.
+// (a TMA or MMA that never completes): record who waited (dwm_hang_info, a
+// device global a debugger or cudaMemcpyFromSymbol can read) and trap
+// instead of hanging the GPU.  No printf here: a call on this path makes
+// ptxas spill registers around it inside every pipeline loop.
+static __device__ unsigned int dwm_hang_info[4];
+static __device__ __noinline__ void mbar_timeout(uint32_t phase) {
+  dwm_hang_info[0] = blockIdx.x;
+  dwm_hang_info[1] = threadIdx.x;
+  dwm_hang_info[2] = phase;
+  dwm_hang_info[3] = 0xDEADu;
+  __threadfence_system();
+  __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   if (mbar_try_wait(bar, phase)) return;
   const uint64_t t0 = globaltimer_ns();
   for (uint32_t polls = 1; !mbar_try_wait(bar, phase); ++polls) {
-    if ((polls & 1023u) == 0 && globaltimer_ns() - t0 > 2000000000ull) {
-      printf("dwm: mbarrier wait timeout (block %d thread %d phase %u)\n", blockIdx.x, threadIdx.x, phase);
-      __trap();
-    }
+    if ((polls & 1023u) == 0 && globaltimer_ns() - t0 > 2000000000ull) mbar_timeout(phase);
   }
 }
 
