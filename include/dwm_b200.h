@@ -132,6 +132,13 @@ int dwm_conv2d_small_c(const dwm_desc_t* desc, const void* x, const void* U,
 size_t dwm_filter_bytes(const dwm_desc_t* desc, int dtype, int algo);
 int dwm_prepare_filter(const dwm_desc_t* desc, int dtype, int algo, const void* w,
                        void* U, void* stream);
+/* dwm_prepare_filter on a strided weight view: strides[4] are the element
+ * strides of (f, c, kh, kw) (any sign; w points at element (0,0,0,0) of the
+ * view).  The backward's data gradient uses it for the channel-transposed,
+ * tap-reversed polyphase sub-kernels w[:, :, rho::s_h, sig::s_w] without
+ * materialising them. */
+int dwm_prepare_filter_strided(const dwm_desc_t* desc, int dtype, int algo, const void* w,
+                               const int64_t* strides, void* U, void* stream);
 int dwm_conv2d_forward_prepared(const dwm_desc_t* desc, int dtype, int algo, const void* x,
                                 const void* U, void* y, void* workspace, size_t workspace_bytes,
                                 int32_t* nonfinite_flag, void* stream);
@@ -147,11 +154,13 @@ int dwm_conv2d_forward_prepared(const dwm_desc_t* desc, int dtype, int algo, con
  *   DWM_ALGO_EXACT (any shape, float64): implicit-im2col GEMM on CUDA cores,
  *                  geometry-fixed split-K, fixed-order partial sums.
  * Both deterministic.  workspace >= dwm_weight_grad_workspace_bytes (may be
- * 0 -> NULL allowed).  (The data gradient is computed by the forward engines
+ * 0 -> NULL allowed).  nonfinite_flag (device int32, may be NULL) is set to 1
+ * when any gradient entry is NaN/Inf.  (The data gradient is computed by the forward engines
  * on the polyphase adjoint problems, see engines.py.) */
 size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* desc, int dtype, int algo);
 int dwm_weight_grad(const dwm_desc_t* desc, int dtype, int algo, const void* x, const void* dy,
-                    void* gw, void* workspace, size_t workspace_bytes, void* stream);
+                    void* gw, void* workspace, size_t workspace_bytes, int32_t* nonfinite_flag,
+                    void* stream);
 
 /* Whole forward: y[N,F,OH,OW] = dwm_conv2d(x[N,C,H,W], w[F,C,r_h,r_w]).
  * nonfinite_flag (device int32, may be NULL) is set to 1 when any output

@@ -22,7 +22,7 @@ ALGO_NAMES = {v: k for k, v in ALGOS.items()}
 EXPORTED_SYMBOLS = (
     "dwm_desc_init", "dwm_elementwise_count", "dwm_workspace_bytes", "dwm_select_algo",
     "dwm_filter_transform", "dwm_input_transform", "dwm_gemm_output",
-    "dwm_filter_bytes", "dwm_prepare_filter", "dwm_conv2d_forward_prepared", "dwm_weight_grad_workspace_bytes", "dwm_weight_grad",
+    "dwm_filter_bytes", "dwm_prepare_filter", "dwm_prepare_filter_strided", "dwm_conv2d_forward_prepared", "dwm_weight_grad_workspace_bytes", "dwm_weight_grad",
     "dwm_conv2d_small_c", "dwm_conv2d_forward", "dwm_last_error", "dwm_version",
 )
 
@@ -98,11 +98,13 @@ def load(required: bool = True):
     lib.dwm_filter_bytes.restype = ctypes.c_size_t
     lib.dwm_prepare_filter.argtypes = [D, I, I, P, P, P]
     lib.dwm_prepare_filter.restype = I
+    lib.dwm_prepare_filter_strided.argtypes = [D, I, I, P, ctypes.POINTER(ctypes.c_int64), P, P]
+    lib.dwm_prepare_filter_strided.restype = I
     lib.dwm_conv2d_forward_prepared.argtypes = [D, I, I, P, P, P, P, ctypes.c_size_t, P, P]
     lib.dwm_conv2d_forward_prepared.restype = I
     lib.dwm_weight_grad_workspace_bytes.argtypes = [D, I, I]
     lib.dwm_weight_grad_workspace_bytes.restype = S
-    lib.dwm_weight_grad.argtypes = [D, I, I, P, P, P, P, S, P]
+    lib.dwm_weight_grad.argtypes = [D, I, I, P, P, P, P, S, P, P]
     lib.dwm_weight_grad.restype = I
     lib.dwm_conv2d_small_c.argtypes = [D, P, P, P, P, P]
     lib.dwm_conv2d_small_c.restype = I

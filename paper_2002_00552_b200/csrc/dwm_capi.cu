@@ -184,6 +184,14 @@ size_t dwm_workspace_bytes(const dwm_desc_t* d, int dtype, int algo) {
   return round_up(v, 256) + round_up(u, 256);
 }
 
+// Workspace-type buffers (V, U, ws) are read with 16-byte vector loads and
+// TMA, which need 16-byte aligned bases; x, w and y only need natural
+// alignment (the kernels pick vector paths at run time when they can).
+static int check_aligned(const void* p, const char* name) {
+  if ((uintptr_t)p & 15u) return fail(DWM_EINVAL_SHAPE, "%s must be 16-byte aligned (got %p)", name, p);
+  return DWM_OK;
+}
+
 static int check_common(const dwm_desc_t* d, int dtype) {
   if (!d) return fail(DWM_EINVAL_SHAPE, "descriptor pointer is NULL");
   if (dtype != DWM_F32 && dtype != DWM_F64)
@@ -195,11 +203,13 @@ static int check_common(const dwm_desc_t* d, int dtype) {
 
 int dwm_filter_transform(const dwm_desc_t* d, int dtype, const void* w, void* U, void* stream) {
   if (int st = check_common(d, dtype)) return st;
+  if (int st = check_aligned(U, "U")) return st;
   return launch_filter_transform(*d, dtype, w, U, (cudaStream_t)stream);
 }
 
 int dwm_input_transform(const dwm_desc_t* d, int dtype, const void* x, void* V, void* stream) {
   if (int st = check_common(d, dtype)) return st;
+  if (int st = check_aligned(V, "V")) return st;
   return launch_input_transform(*d, dtype, x, V, (cudaStream_t)stream);
 }
 
@@ -212,6 +222,8 @@ static int bad_algo(const dwm_desc_t* d, int algo) {
 int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, const void* U,
                     void* y, int32_t* flag, void* ws, size_t ws_bytes, void* stream) {
   if (int st = check_common(d, dtype)) return st;
+  if (int st = check_aligned(V, "V")) return st;
+  if (int st = check_aligned(U, "U")) return st;
   int sel = dwm_select_algo(d, dtype, algo);
   if (sel == DWM_ALGO_SMALL_C) sel = algo == DWM_ALGO_AUTO ? DWM_ALGO_EXACT : -1;
   if (sel < 0) return bad_algo(d, algo);
@@ -240,19 +252,22 @@ size_t dwm_weight_grad_workspace_bytes(const dwm_desc_t* d, int dtype, int algo)
 }
 
 int dwm_weight_grad(const dwm_desc_t* d, int dtype, int algo, const void* x, const void* dy, void* gw, void* ws,
-                    size_t ws_bytes, void* stream) {
+                    size_t ws_bytes, int32_t* flag, void* stream) {
   if (int st = check_common(d, dtype)) return st;
+  if (ws_bytes > 0)
+    if (int st = check_aligned(ws, "workspace")) return st;
   const int sel = wgrad_select(d, dtype, algo);
   if (sel < 0)
     return fail(DWM_EUNSUPPORTED, "weight-gradient engine %d not available (tcgen05: float32, C %% 32 == 0, "
                 "C >= 64, F >= 64; got C=%d F=%d)", algo, d->c, d->f);
-  if (sel == DWM_ALGO_TC) return launch_wgrad_tc(*d, x, dy, gw, ws, ws_bytes, (cudaStream_t)stream);
-  return launch_weight_grad(*d, dtype, x, dy, gw, ws, ws_bytes, (cudaStream_t)stream);
+  if (sel == DWM_ALGO_TC) return launch_wgrad_tc(*d, x, dy, gw, ws, ws_bytes, flag, (cudaStream_t)stream);
+  return launch_weight_grad(*d, dtype, x, dy, gw, ws, ws_bytes, flag, (cudaStream_t)stream);
 }
 
 int dwm_conv2d_small_c(const dwm_desc_t* d, const void* x, const void* U, void* y, int32_t* flag,
                        void* stream) {
   if (int st = check_common(d, DWM_F32)) return st;
+  if (int st = check_aligned(U, "U")) return st;
   if (!small_c_supported(*d)) return bad_algo(d, DWM_ALGO_SMALL_C);
   return launch_small_c(*d, x, U, y, flag, (cudaStream_t)stream);
 }
@@ -265,6 +280,7 @@ int dwm_conv2d_forward(const dwm_desc_t* d, int dtype, int algo, const void* x, 
   const size_t need = dwm_workspace_bytes(d, dtype, sel);
   if (!ws || ws_bytes < need)
     return fail(DWM_EINVAL_SHAPE, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
+  if (int st2 = check_aligned(ws, "workspace")) return st2;
   const size_t es = dtype == DWM_F64 ? 8 : 4;
   char* base = (char*)ws;
   void* V = base;
@@ -292,10 +308,22 @@ size_t dwm_filter_bytes(const dwm_desc_t* d, int dtype, int algo) {
 
 int dwm_prepare_filter(const dwm_desc_t* d, int dtype, int algo, const void* w, void* U, void* stream) {
   if (int st = check_common(d, dtype)) return st;
+  if (int st = check_aligned(U, "U")) return st;
   const int sel = dwm_select_algo(d, dtype, algo);
   if (sel < 0) return bad_algo(d, algo);
   if (sel == DWM_ALGO_TC) return launch_filter_transform_tf32split(*d, w, U, (cudaStream_t)stream);
   return launch_filter_transform(*d, dtype, w, U, (cudaStream_t)stream);
+}
+
+int dwm_prepare_filter_strided(const dwm_desc_t* d, int dtype, int algo, const void* w, const int64_t* strides,
+                               void* U, void* stream) {
+  if (int st = check_common(d, dtype)) return st;
+  if (!strides) return fail(DWM_EINVAL_SHAPE, "strides pointer is NULL");
+  if (int st = check_aligned(U, "U")) return st;
+  const int sel = dwm_select_algo(d, dtype, algo);
+  if (sel < 0) return bad_algo(d, algo);
+  if (sel == DWM_ALGO_TC) return launch_filter_transform_tf32split(*d, w, U, (cudaStream_t)stream, strides);
+  return launch_filter_transform(*d, dtype, w, U, (cudaStream_t)stream, strides);
 }
 
 int dwm_conv2d_forward_prepared(const dwm_desc_t* d, int dtype, int algo, const void* x, const void* U,
@@ -304,10 +332,15 @@ int dwm_conv2d_forward_prepared(const dwm_desc_t* d, int dtype, int algo, const 
   const int sel = dwm_select_algo(d, dtype, algo);
   if (sel < 0) return bad_algo(d, algo);
   cudaStream_t s = (cudaStream_t)stream;
-  if (sel == DWM_ALGO_SMALL_C) return launch_small_c(*d, x, U, y, flag, s);
+  int st0;
+  if (sel == DWM_ALGO_SMALL_C) {
+    if ((st0 = check_aligned(U, "U"))) return st0;
+    return launch_small_c(*d, x, U, y, flag, s);
+  }
   const size_t need = v_bytes_of(d, dtype == DWM_F64 ? 8 : 4);
   if (!ws || ws_bytes < need)
     return fail(DWM_EINVAL_SHAPE, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
+  if ((st0 = check_aligned(ws, "workspace")) || (st0 = check_aligned(U, "U"))) return st0;
   int st;
   if ((st = launch_input_transform(*d, dtype, x, ws, s))) return st;
   if (sel == DWM_ALGO_TC) return launch_gemm_tc(*d, ws, U, y, flag, s);

@@ -20,8 +20,19 @@ namespace dwm {
 // ---------------------------------------------------------------------------
 // Filter transform: one thread per (f, c); U[fq][f][c].
 // ---------------------------------------------------------------------------
+// Element strides of the weight view the filter transforms read: (f, c, kh, kw).
+// The forward passes the contiguous F,C,r_h,r_w layout; the backward's data
+// gradient passes the channel-transposed, tap-reversed polyphase sub-kernels
+// w[:, :, rho::s_h, sig::s_w] (negative tap strides) without materialising them.
+struct FiltView {
+  int64_t sf, sc, skh, skw;
+};
+__host__ __device__ inline FiltView contiguous_view(const dwm_desc_t& d) {
+  return FiltView{(int64_t)d.c * d.r_h * d.r_w, (int64_t)d.r_h * d.r_w, d.r_w, 1};
+}
+
 template <typename T>
-__device__ __forceinline__ void part_filter_transform(const dwm_desc_t& d, const T* __restrict__ wfc,
+__device__ __forceinline__ void part_filter_transform(const dwm_desc_t& d, const T* __restrict__ wfc, const FiltView& fv,
                                                       int rp, int cp, T out[4][4]) {
   const dwm_axis_part_t R = d.row_parts[rp], Cc = d.col_parts[cp];
   const int pr = R.count, pc = Cc.count;
@@ -30,7 +41,9 @@ __device__ __forceinline__ void part_filter_transform(const dwm_desc_t& d, const
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      g[i][j] = (i < pr && j < pc) ? wfc[(R.origin + R.step * i) * d.r_w + Cc.origin + Cc.step * j] : T(0);
+      g[i][j] = (i < pr && j < pc)
+                    ? wfc[(int64_t)(R.origin + R.step * i) * fv.skh + (int64_t)(Cc.origin + Cc.step * j) * fv.skw]
+                    : T(0);
   // row stage: t[u][j] = sum_i G_r[u][i] * g[i][j]
   T t[4][3];
 #pragma unroll
@@ -57,16 +70,17 @@ __device__ __forceinline__ void part_filter_transform(const dwm_desc_t& d, const
 }
 
 template <typename T>
-__global__ void filter_transform_kernel(const dwm_desc_t d, const T* __restrict__ w, T* __restrict__ U) {
+__global__ void filter_transform_kernel(const dwm_desc_t d, const T* __restrict__ w, const FiltView fv,
+                                        T* __restrict__ U) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t fc = (int64_t)d.f * d.c;
   if (idx >= fc) return;
-  const T* wfc = w + idx * d.r_h * d.r_w;  // idx = f*C + c
+  const T* wfc = w + (idx / d.c) * fv.sf + (idx % d.c) * fv.sc;  // idx = f*C + c
   int fq = 0;
   for (int rp = 0; rp < d.n_row_parts; ++rp)
     for (int cp = 0; cp < d.n_col_parts; ++cp) {
       T u[4][4];
-      part_filter_transform(d, wfc, rp, cp, u);
+      part_filter_transform(d, wfc, fv, rp, cp, u);
       const int lr = d.row_parts[rp].count + 1, lc = d.col_parts[cp].count + 1;
 #pragma unroll
       for (int a = 0; a < 4; ++a)
@@ -86,7 +100,7 @@ __device__ __forceinline__ float tf32_rn(float x) {
 // U_hi = tf32(U), U_lo = tf32(U - U_hi), stacked per 64-filter block:
 // U[((fq * nblk + f / 64) * 128 + {0: hi, 64: lo} + f % 64) * C + c]; one
 // thread per (f, c) over the padded filter count (rows past F are zeros).
-__global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const float* __restrict__ w,
+__global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const float* __restrict__ w, const FiltView fv,
                                                   float* __restrict__ U) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int nblk = (d.f + 63) / 64;
@@ -94,13 +108,13 @@ __global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const floa
   if (idx >= fcp) return;
   const int f = (int)(idx / d.c), c = (int)(idx % d.c);
   const bool live = f < d.f;
-  const float* wfc = w + (live ? (int64_t)f * d.c + c : 0) * d.r_h * d.r_w;
+  const float* wfc = w + (live ? (int64_t)f * fv.sf + (int64_t)c * fv.sc : 0);
   const int64_t row0 = (int64_t)(f / 64) * 128 + f % 64;
   int fq = 0;
   for (int rp = 0; rp < d.n_row_parts; ++rp)
     for (int cp = 0; cp < d.n_col_parts; ++cp) {
       float u[4][4];
-      part_filter_transform(d, wfc, rp, cp, u);
+      part_filter_transform(d, wfc, fv, rp, cp, u);
       const int lr = d.row_parts[rp].count + 1, lc = d.col_parts[cp].count + 1;
 #pragma unroll
       for (int a = 0; a < 4; ++a)
@@ -389,19 +403,23 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 
 static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
-int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s) {
+int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s,
+                            const int64_t* strides) {
   const int64_t n = (int64_t)d.f * d.c;
+  const FiltView fv = strides ? FiltView{strides[0], strides[1], strides[2], strides[3]} : contiguous_view(d);
   if (dtype == DWM_F64)
-    filter_transform_kernel<double><<<grid_for(n, 128), 128, 0, s>>>(d, (const double*)w, (double*)U);
+    filter_transform_kernel<double><<<grid_for(n, 128), 128, 0, s>>>(d, (const double*)w, fv, (double*)U);
   else
-    filter_transform_kernel<float><<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, (float*)U);
+    filter_transform_kernel<float><<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, fv, (float*)U);
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }
 
-int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s) {
+int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s,
+                                      const int64_t* strides) {
   const int64_t n = (int64_t)((d.f + 63) / 64) * 64 * d.c;
-  filter_transform_tf32split_kernel<<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, (float*)U);
+  const FiltView fv = strides ? FiltView{strides[0], strides[1], strides[2], strides[3]} : contiguous_view(d);
+  filter_transform_tf32split_kernel<<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, fv, (float*)U);
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }
@@ -499,7 +517,7 @@ namespace dwm {
 template <typename T>
 __global__ void __launch_bounds__(256) weight_grad_kernel(const dwm_desc_t d, const T* __restrict__ x,
                                                           const T* __restrict__ dy, T* __restrict__ gw,
-                                                          int64_t seg_len) {
+                                                          int64_t seg_len, int32_t* __restrict__ flag) {
   constexpr int BM = 64, BN = 64, BK = 16;
   __shared__ __align__(16) T As[BK][BM];
   __shared__ __align__(16) T Bs[BK][BN];
@@ -615,7 +633,11 @@ __global__ void __launch_bounds__(256) weight_grad_kernel(const dwm_desc_t d, co
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int j = j0 + tx * 4 + v;
-      if (j < ncols) gw[(int64_t)f * ncols + j] = add_rn(tot[u][v], mid[u][v]);
+      if (j < ncols) {
+        const T g = add_rn(tot[u][v], mid[u][v]);
+        gw[(int64_t)f * ncols + j] = g;
+        if (flag && !isfinite(g)) *flag = 1;  // (only the unsplit launch passes a flag)
+      }
     }
   }
 }
@@ -623,12 +645,13 @@ __global__ void __launch_bounds__(256) weight_grad_kernel(const dwm_desc_t d, co
 // Fixed-order sum of the split-K partials (segment 0 first).
 template <typename T>
 __global__ void weight_grad_reduce_kernel(const T* __restrict__ part, T* __restrict__ gw, int64_t count,
-                                          int splits) {
+                                          int splits, int32_t* __restrict__ flag) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   T v = part[i];
   for (int z = 1; z < splits; ++z) v = add_rn(v, part[(int64_t)z * count + i]);
   gw[i] = v;
+  if (flag && !isfinite(v)) *flag = 1;
 }
 
 // Split count from the geometry only (never from the device), so a given
@@ -644,7 +667,7 @@ int weight_grad_splits(const dwm_desc_t& d) {
 }
 
 int launch_weight_grad(const dwm_desc_t& d, int dtype, const void* x, const void* dy, void* gw, void* ws,
-                       size_t ws_bytes, cudaStream_t s) {
+                       size_t ws_bytes, int32_t* flag, cudaStream_t s) {
   const int ncols = d.c * d.r_h * d.r_w;
   const int splits = weight_grad_splits(d);
   const int64_t K = (int64_t)d.n * d.oh * d.ow;
@@ -658,11 +681,15 @@ int launch_weight_grad(const dwm_desc_t& d, int dtype, const void* x, const void
   void* dst = splits > 1 ? ws : gw;
   const unsigned rg = (unsigned)((count + 255) / 256);
   if (dtype == DWM_F64) {
-    weight_grad_kernel<double><<<grid, 256, 0, s>>>(d, (const double*)x, (const double*)dy, (double*)dst, seg);
-    if (splits > 1) weight_grad_reduce_kernel<double><<<rg, 256, 0, s>>>((const double*)ws, (double*)gw, count, splits);
+    weight_grad_kernel<double><<<grid, 256, 0, s>>>(d, (const double*)x, (const double*)dy, (double*)dst, seg,
+                                                     splits > 1 ? nullptr : flag);
+    if (splits > 1)
+      weight_grad_reduce_kernel<double><<<rg, 256, 0, s>>>((const double*)ws, (double*)gw, count, splits, flag);
   } else {
-    weight_grad_kernel<float><<<grid, 256, 0, s>>>(d, (const float*)x, (const float*)dy, (float*)dst, seg);
-    if (splits > 1) weight_grad_reduce_kernel<float><<<rg, 256, 0, s>>>((const float*)ws, (float*)gw, count, splits);
+    weight_grad_kernel<float><<<grid, 256, 0, s>>>(d, (const float*)x, (const float*)dy, (float*)dst, seg,
+                                                   splits > 1 ? nullptr : flag);
+    if (splits > 1)
+      weight_grad_reduce_kernel<float><<<rg, 256, 0, s>>>((const float*)ws, (float*)gw, count, splits, flag);
   }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;

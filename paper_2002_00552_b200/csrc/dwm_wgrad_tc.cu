@@ -266,7 +266,8 @@ __global__ void grad_out_transform_kernel(const dwm_desc_t d, int64_t t_pad, con
 }
 
 // gw[f][c][taps of part] = G_r^T dU_part G_c, placed at the part's strided taps.
-__global__ void wgrad_place_kernel(const dwm_desc_t d, const float* __restrict__ du, float* __restrict__ gw) {
+__global__ void wgrad_place_kernel(const dwm_desc_t d, const float* __restrict__ du, float* __restrict__ gw,
+                                   int32_t* __restrict__ flag) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)d.f * d.c) return;
   const int c = (int)(idx % d.c), f = (int)(idx / d.c);
@@ -288,6 +289,7 @@ __global__ void wgrad_place_kernel(const dwm_desc_t d, const float* __restrict__
             acc = fmaf(c_g[pr][a][i], row, acc);
           }
           g[(R.origin + R.step * i) * d.r_w + Cc.origin + Cc.step * j] = acc;
+          if (flag && !isfinite(acc)) *flag = 1;
         }
       q += lr * lc;
     }
@@ -333,7 +335,7 @@ size_t wgrad_tc_workspace_bytes(const dwm_desc_t& d) {
 }
 
 int launch_wgrad_tc(const dwm_desc_t& d, const void* x, const void* dy, void* gw, void* ws, size_t ws_bytes,
-                    cudaStream_t s) {
+                    int32_t* flag, cudaStream_t s) {
   if (!wgrad_tc_supported(d)) return fail(DWM_EUNSUPPORTED, "tcgen05 weight gradient needs C %% 32 == 0, C, F >= 64");
   if (!ws || ws_bytes < wgrad_tc_workspace_bytes(d))
     return fail(DWM_EINVAL_SHAPE, "weight-gradient workspace too small: %zu bytes given, %zu needed", ws_bytes,
@@ -376,7 +378,7 @@ int launch_wgrad_tc(const dwm_desc_t& d, const void* x, const void* dy, void* gw
   wgrad_tc_kernel<<<grid, THREADS, smem, s>>>(d, tp, mv, mh, ml, du);
   DWM_CUDA_TRY(cudaGetLastError());
   const int64_t fc = (int64_t)d.f * d.c;
-  wgrad_place_kernel<<<(unsigned)((fc + 127) / 128), 128, 0, s>>>(d, du, (float*)gw);
+  wgrad_place_kernel<<<(unsigned)((fc + 127) / 128), 128, 0, s>>>(d, du, (float*)gw, flag);
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }

@@ -18,6 +18,7 @@ reference's test mode is not (TypeError).  There is no CPU fallback: without
 the native library or a CUDA device every call raises.
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -365,38 +366,64 @@ def _phase_geometry(rho: int, s: int, r: int, pad_lo: int, size: int, out: int):
     return taps, i_min, m, lo, hi
 
 
-def _data_grad_polyphase(dy, wt, spec: ConvSpec, hw, algo: str, stream):
+def _data_grad_polyphase(dy, wt, spec: ConvSpec, hw, algo: str, stream, flag):
     """Input gradient as s_h*s_w stride-1 DWM forwards (one per output phase):
     grad_pad[s*i + rho] = sum_t dY[i - t] * w[rho + s*t]  -- the DWM stride
     split applied to the adjoint, so no zero-inserted (dilated) grad_out and no
-    multiply by an inserted zero.  Phases write disjoint positions."""
+    multiply by an inserted zero.  Phases write disjoint positions.
+
+    Each phase's filter is the channel-transposed, tap-reversed sub-kernel
+    w[:, :, rho::s_h, sig::s_w]: its transform reads it in place through
+    element strides (dwm_prepare_filter_strided), nothing is materialised.
+    A stride-1 problem has one phase covering the whole gradient, written
+    directly; the non-finite flag of every phase accumulates in ``flag``
+    (one device->host read for the whole backward)."""
     torch = _torch()
+    lib = _native.load()
     n, f, oh, ow = dy.shape
     c = wt.shape[1]
     h, w = hw
     r_h, r_w = spec.kernel
     s_h, s_w = spec.stride
     top, _, left, _ = spec.pad
+    code = _native.DWM_F64 if dy.dtype == torch.float64 else _native.DWM_F32
+    algo_code = _native.ALGOS[algo]
     rows = [_phase_geometry(rho, s_h, r_h, top, h, oh) for rho in range(s_h)]
     cols = [_phase_geometry(sig, s_w, r_w, left, w, ow) for sig in range(s_w)]
     covered = all(g[0] > 0 for g in rows + cols)
     gd = (torch.empty if covered else torch.zeros)((n, c, h, w), dtype=dy.dtype, device=dy.device)
-    w_t = wt.transpose(0, 1)  # (C, F, r_h, r_w)
+    wc = wt.contiguous()
     for rho, (tr, i0, m, pt, pb) in enumerate(rows):
         if tr == 0 or m <= 0:
             continue
         for sig, (tc, j0, mc, pl, pr) in enumerate(cols):
             if tc == 0 or mc <= 0:
                 continue
-            sub = w_t[:, :, rho::s_h, sig::s_w].flip(2, 3).contiguous()  # (C, F, tr, tc)
             src = dy
             if min(pt, pb, pl, pr) < 0:
-                src = dy[:, :, max(0, -pt):oh - max(0, -pb), max(0, -pl):ow - max(0, -pr)]
+                src = dy[:, :, max(0, -pt):oh - max(0, -pb), max(0, -pl):ow - max(0, -pr)].contiguous()
             adj = ConvSpec(kernel=(tr, tc), stride=(1, 1),
                            pad=(max(0, pt), max(0, pb), max(0, pl), max(0, pr)))
-            y = dwm_conv2d(src.contiguous(), sub, adj, algo=algo, check_finite=False, stream=stream)
+            # the phase problem: data = grad_out (F channels), filters = C
+            desc = _native.make_desc(n, f, src.shape[2], src.shape[3], c, adj.kernel, adj.stride, adj.pad)
+            # element (c', f', i, j) of the reversed sub-kernel is
+            # w[f', c', rho + s_h*(tr-1-i), sig + s_w*(tc-1-j)]
+            base = wc[0, 0, rho + s_h * (tr - 1), sig + s_w * (tc - 1)]
+            strides = (ctypes.c_int64 * 4)(r_h * r_w, c * r_h * r_w, -s_h * r_w, -s_w)
+            u = _workspace(lib.dwm_filter_bytes(desc, code, algo_code), dy.device)
+            _native.check(lib.dwm_prepare_filter_strided(desc, code, algo_code, base.data_ptr(), strides,
+                                                         u.data_ptr(), stream.cuda_stream),
+                          "dwm_prepare_filter_strided")
             r0, c0 = s_h * i0 + rho - top, s_w * j0 + sig - left
-            gd[:, :, r0::s_h, c0::s_w] = y
+            direct = (s_h, s_w) == (1, 1) and (r0, c0) == (0, 0) and (desc.oh, desc.ow) == (h, w)
+            y = gd if direct else torch.empty((n, c, desc.oh, desc.ow), dtype=dy.dtype, device=dy.device)
+            ws_bytes = lib.dwm_workspace_bytes(desc, code, algo_code)
+            ws = _workspace(ws_bytes, dy.device)
+            _native.check(lib.dwm_conv2d_forward_prepared(desc, code, algo_code, src.data_ptr(), u.data_ptr(),
+                                                          y.data_ptr(), ws.data_ptr(), ws_bytes, flag.data_ptr(),
+                                                          stream.cuda_stream), "dwm_conv2d_forward_prepared")
+            if not direct:
+                gd[:, :, r0::s_h, c0::s_w] = y
     return gd
 
 
@@ -460,6 +487,8 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
             x = _to_device(data, dev, tdt)
             wt = _to_device(weights, dev, tdt)
 
+            # one device flag for every kernel of the backward, read once
+            flag = torch.zeros(1, dtype=torch.int32, device=dev)
             gw = None
             if need_weights:
                 gw = torch.empty((f, c, r_h, r_w), dtype=tdt, device=dev)
@@ -468,12 +497,12 @@ def dwm_backward(grad_out, plan: DecompositionPlan, data, weights, precision=Non
                 wg_bytes = int(lib.dwm_weight_grad_workspace_bytes(desc, code, wg_algo))
                 wg_ws = _workspace(wg_bytes, dev)
                 _native.check(lib.dwm_weight_grad(desc, code, wg_algo, x.data_ptr(), dy.data_ptr(),
-                                                  gw.data_ptr(), wg_ws.data_ptr(), wg_bytes, s.cuda_stream),
+                                                  gw.data_ptr(), wg_ws.data_ptr(), wg_bytes, flag.data_ptr(),
+                                                  s.cuda_stream),
                               "dwm_weight_grad")
-            gd = _data_grad_polyphase(dy, wt, spec, (h, w), algo, s) if need_data else None
-            for g in (gd, gw):
-                if g is not None and not bool(torch.isfinite(g).all()):
-                    raise FloatingPointError("dwm_backward produced non-finite values")
+            gd = _data_grad_polyphase(dy, wt, spec, (h, w), algo, s, flag) if need_data else None
+            if int(flag.item()) != 0:
+                raise FloatingPointError("dwm_backward produced non-finite values")
     if not _is_torch(grad_out):
         return tuple(None if g is None else g.cpu().numpy() for g in (gd, gw))
     if not cuda_in:

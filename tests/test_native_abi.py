@@ -84,3 +84,15 @@ def test_native_errors_mirror_reference_messages():
     assert st == _native.DWM_EINVAL_DTYPE
     st = lib.dwm_conv2d_forward(d, 0, 0, None, None, None, None, 0, None, None)
     assert st == _native.DWM_EINVAL_SHAPE and b"not initialised" in lib.dwm_last_error()
+
+
+def test_workspace_pointers_must_be_16_byte_aligned():
+    """V/U/workspace operands are read by 16-byte vectors and TMA: a
+    misaligned pointer is rejected before any launch (no device needed)."""
+    from paper_2002_00552_b200 import _native
+    lib = _native.load()
+    d = _native.make_desc(1, 32, 8, 8, 16, (3, 3), (1, 1), (1, 1, 1, 1))
+    st = lib.dwm_filter_transform(d, _native.DWM_F32, 0x1000, 0x1004, None)
+    assert st == _native.DWM_EINVAL_SHAPE and "16-byte aligned" in _native.last_error()
+    st = lib.dwm_input_transform(d, _native.DWM_F32, 0x1000, 0x1008, None)
+    assert st == _native.DWM_EINVAL_SHAPE

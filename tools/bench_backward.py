@@ -47,7 +47,7 @@ def main():
         def wgrad():
             _native.check(lib.dwm_weight_grad(desc, _native.DWM_F32, wg_algo, x.data_ptr(), dy.data_ptr(),
                                               gw.data_ptr(),
-                                              wg_ws.data_ptr(), wg_bytes, torch.cuda.current_stream().cuda_stream))
+                                              wg_ws.data_ptr(), wg_bytes, None, torch.cuda.current_stream().cuda_stream))
 
         def full():
             dwm_backward(dy, plan, x, w, wgrad_algo=args.wgrad_algo)

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <string>
 #include <vector>
 
 #include "../paper_2002_00552_b200/csrc/dwm_sm100.cuh"
@@ -388,8 +390,52 @@ void rate(int sms) {
   cudaFree(sink);
 }
 
-int main() {
+// Sustained rate: the N = 256 SS loop launched back to back for ~4 s (the
+// regime of a long GEMM under the board power limit; MEASURED_PEAKS.json's
+// bf16 "sustained" figure is measured the same way).  Reports the median of
+// the last second's launches and the median SM clock sampled by nvidia-smi
+// is left to the caller.
+template <int N>
+void rate_sustained(int sms, double seconds) {
+  float* sink;
+  cudaMalloc(&sink, 4 * 1024);
+  const int smem = 1024 + (128 + N) * 128;
+  cudaFuncSetAttribute(mma_rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 4000;
+  const double flops = 2.0 * 128 * N * 32 * (double)iters * sms;
+  std::vector<float> ms_all;
+  double total = 0;
+  while (total < seconds * 1e3) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    mma_rate<N><<<sms, 128, smem>>>(iters, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms_all.push_back(ms);
+    total += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  std::vector<float> tail(ms_all.end() - ms_all.size() / 4, ms_all.end());
+  std::sort(tail.begin(), tail.end());
+  const float med = tail[tail.size() / 2];
+  printf("tf32 MMA M=128 N=%3d K=8 (SS) sustained %.1f s: last-quarter median %.3f ms  %.1f TFLOP/s\n", N,
+         total / 1e3, med, flops / med / 1e9);
+  cudaFree(sink);
+}
+
+int main(int argc, char** argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
+  if (argc > 1 && std::string(argv[1]) == "--sustained") {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    rate_sustained<256>(sms, 4.0);
+    return 0;
+  }
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int bad = 0;
