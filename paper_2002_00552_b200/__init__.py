@@ -13,3 +13,4 @@ from .transforms import TransformSet, get_transform, precision_dtype, to_float
 
 __version__ = "0.1.0"
 from .module import DWMConv2d, DWMConv2dFunction, FilterCache, dwm_conv2d_op  # noqa: E402
+from .graphs import DWMConvGraph  # noqa: E402

@@ -19,6 +19,7 @@ the native library or a CUDA device every call raises.
 """
 
 import ctypes
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -125,12 +126,17 @@ def _aligned(t):
     return t if t.data_ptr() % 16 == 0 else t.clone()
 
 
+_SMALL_WORKSPACE = 256 << 20
+
+
 def _batch_chunk(lib, desc, code, algo_code, spec, dev, budget=None) -> int:
     """Largest batch chunk whose workspace fits the device memory budget
     (free memory plus torch's cached-but-unused blocks, with 20 % headroom);
     the whole batch when it fits."""
     n = desc.n
     need = lib.dwm_workspace_bytes(desc, code, algo_code)
+    if budget is None and need <= _SMALL_WORKSPACE:
+        return max(n, 1)  # no device-memory query on the small-problem path
     if budget is None:
         torch = _torch()
         free, _ = torch.cuda.mem_get_info(dev)
@@ -183,6 +189,24 @@ def _axis_parts_of(plan):
     return rows, cols
 
 
+@functools.lru_cache(maxsize=256)
+def _cached_plan(spec: ConvSpec) -> DecompositionPlan:
+    return plan_decomposition(spec)
+
+
+@functools.lru_cache(maxsize=256)
+def _cached_desc_key(n, c, h, w, f, kernel, stride, pad):
+    d = _native.make_desc(n, c, h, w, f, kernel, stride, pad)
+    # the native planner must agree with the host planner for this spec (checked once per geometry)
+    _check_plan_matches(_cached_plan(ConvSpec(kernel=kernel, stride=stride, pad=pad)), d)
+    return d
+
+
+def _cached_desc(n, c, h, w, f, spec: ConvSpec):
+    """Descriptor per geometry (read-only once built: the C ABI takes it by const pointer)."""
+    return _cached_desc_key(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
+
+
 def _check_plan_matches(plan, desc) -> None:
     rows, cols = _axis_parts_of(plan)
     if rows != desc.axis("row") or cols != desc.axis("col"):
@@ -206,8 +230,9 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
     spec = _as_spec(spec)
     if tuple(weights.shape[2:]) != spec.kernel:
         raise ValueError(f"weights taps {tuple(weights.shape[2:])} do not match kernel {spec.kernel}")
-    if plan is None:
-        plan = plan_decomposition(spec)
+    own_plan = plan is None
+    if own_plan:
+        plan = _cached_plan(spec)
     else:
         _check_plan(plan, spec)
     dt = _np_dtype(data) if precision is None else precision_dtype(precision)
@@ -225,8 +250,9 @@ def dwm_conv2d(data, weights, spec: ConvSpec, plan: DecompositionPlan = None,
     lib = _native.load()
     # host-side planning first (pure C++, no device): the native planner's
     # axis parts must be the caller's plan
-    desc = _native.make_desc(n, c, h, w, f, spec.kernel, spec.stride, spec.pad)
-    _check_plan_matches(plan, desc)
+    desc = _cached_desc(n, c, h, w, f, spec)
+    if not own_plan:
+        _check_plan_matches(plan, desc)
     if not torch.cuda.is_available():
         raise _native.NativeError("dwm_conv2d needs a CUDA device (B200); there is no CPU fallback")
     tdt = torch.float64 if dt == np.dtype(np.float64) else torch.float32

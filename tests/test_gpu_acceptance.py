@@ -196,3 +196,24 @@ def test_reference_objects_on_gpu(cuda, ref):
                             plan=ref.plan_decomposition(rspec))
         assert np.array_equal(ours, theirs)
         assert mse(theirs, direct_conv2d_f64(d, g, wl.spec())) <= BASE[name]["dwm32_mse"] * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("name", ["cfg1-5x5s1", "cfg5-3x3s2"])
+def test_graph_path_bit_identical_to_eager(cuda, name):
+    """DWMConvGraph (one CUDA-graph replay per call) gives the eager call's
+    bytes, for device and host inputs, and raises on a non-finite output."""
+    import torch
+    from paper_2002_00552_b200 import DWMConvGraph
+    wl = WORKLOADS[name]
+    n = min(wl.batch, 2)
+    x = torch.randn(n, wl.c_in, wl.hw, wl.hw, device=cuda)
+    w = torch.randn(wl.c_out, wl.c_in, wl.kernel, wl.kernel, device=cuda)
+    want = dwm_conv2d(x, w, wl.spec())
+    g = DWMConvGraph(x.shape, w.shape, wl.spec(), device=cuda)
+    for _ in range(3):
+        assert torch.equal(g(x, w), want)
+    assert torch.equal(g(x.cpu().numpy(), w.cpu()), want)
+    xb = x.clone()
+    xb[0, 0, 3, 3] = float("inf")
+    with pytest.raises(FloatingPointError):
+        g(xb, w)
