@@ -332,6 +332,282 @@ small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __r
   }
 }
 
+// ===========================================================================
+// Warp-specialized variant (round 2): 4 producer warps gather + transform V
+// into a 3-stage shared-memory ring; 8 consumer warps run the channel FMA
+// chains and the At stages with the y accumulators in REGISTERS (no shared-
+// memory read-modify-write per part, no __syncthreads: mbarrier handshakes),
+// register budgets redistributed with setmaxnreg.  Same arithmetic in the
+// same order as small_c_kernel, so the same bits (the reference's).
+// ===========================================================================
+constexpr int WS_CONS = 8, WS_PROD = 4, WS_THREADS = 32 * (WS_CONS + WS_PROD);
+constexpr int WS_STAGES = 3;
+constexpr int WS_REG_CONS = 208, WS_REG_PROD = 80;
+static_assert(WS_CONS * 32 * WS_REG_CONS + WS_PROD * 32 * WS_REG_PROD <= 65536, "register file");
+
+template <int CC_, int TM_, int TN_>
+struct WsCfg {
+  static constexpr int CC = CC_, TM = TM_, TN = TN_;
+  static constexpr int BM = 32 * TM;   // tiles per block (lane = tile)
+  static constexpr int BN = 8 * TN;    // filters per block (consumer warp = filter group)
+  static constexpr int NP = TN / 2;
+  static constexpr int VSTAGE = MAXQ * CC * BM;
+  static constexpr int PPER = (BM * CC + 32 * WS_PROD - 1) / (32 * WS_PROD);  // producer slots per thread
+  static size_t smem_bytes(int num_freqs) {
+    return (WS_STAGES * (size_t)VSTAGE + (size_t)num_freqs * CC * BN) * sizeof(float) + 2 * WS_STAGES * 8 + 16;
+  }
+};
+
+// consume_part with the plan-order aggregation into register accumulators
+template <class K, int PR, int PC>
+__device__ __forceinline__ void consume_part_reg(const float* __restrict__ sV, const float* __restrict__ sU,
+                                                 f2 (&acc)[K::TM][K::NP][2][2], int tm, int tn, bool first_part) {
+  constexpr int LR = PR + 1, LC = PC + 1, TM = K::TM, NP = K::NP, CC = K::CC, BM = K::BM, BN = K::BN;
+  f2 T[TM][NP][2][2];
+  static_for<LC>([&](auto bI) {
+    constexpr int b = decltype(bI)::value;
+    f2 S[TM][NP][2];
+    static_for<LR>([&](auto aI) {
+      constexpr int a = decltype(aI)::value;
+      constexpr int q = a * LC + b;
+      f2 M[TM][NP];
+#pragma unroll
+      for (int c = 0; c < CC; ++c) {
+        float v[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) v[i] = sV[(q * CC + c) * BM + tm + 32 * i];
+        f2 u[NP];
+        const float* up = sU + (q * CC + c) * BN + tn * K::TN;
+#pragma unroll
+        for (int jp = 0; jp < NP; jp += 2) {
+          if (K::TN % 4 == 0 && jp + 1 < NP) {
+            const float4 u4 = *reinterpret_cast<const float4*>(up + 2 * jp);
+            u[jp] = pk(u4.x, u4.y);
+            u[jp + 1] = pk(u4.z, u4.w);
+          } else {
+            const float2 u2 = *reinterpret_cast<const float2*>(up + 2 * jp);
+            u[jp] = pk(u2.x, u2.y);
+            if (jp + 1 < NP) {
+              const float2 u3 = *reinterpret_cast<const float2*>(up + 2 * jp + 2);
+              u[jp + 1] = pk(u3.x, u3.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const f2 vv = pk(v[i], v[i]);
+#pragma unroll
+          for (int jp = 0; jp < NP; ++jp) M[i][jp] = (c == 0) ? mul2(u[jp], vv) : fma2(u[jp], vv, M[i][jp]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int jp = 0; jp < NP; ++jp) {
+          chain2<at_coef(PR, 0, a), (a == at_first(PR, 0))>(S[i][jp][0], M[i][jp]);
+          chain2<at_coef(PR, 1, a), (a == at_first(PR, 1))>(S[i][jp][1], M[i][jp]);
+        }
+    });
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int jp = 0; jp < NP; ++jp)
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii) {
+          chain2<at_coef(PC, 0, b), (b == at_first(PC, 0))>(T[i][jp][ii][0], S[i][jp][ii]);
+          chain2<at_coef(PC, 1, b), (b == at_first(PC, 1))>(T[i][jp][ii][1], S[i][jp][ii]);
+        }
+  });
+  // aggregation in plan order (tensor.py:68-81): acc = acc + T
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int jp = 0; jp < NP; ++jp)
+#pragma unroll
+      for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+          acc[i][jp][ii][jj] = first_part ? T[i][jp][ii][jj] : add2(acc[i][jp][ii][jj], T[i][jp][ii][jj]);
+}
+
+template <uint32_t N>
+__device__ __forceinline__ void ws_setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <uint32_t N>
+__device__ __forceinline__ void ws_setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+
+__device__ __forceinline__ void ws_bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void ws_bar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void ws_bar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+}
+
+template <class K>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+small_c_ws_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __restrict__ U,
+                  float* __restrict__ y, int32_t* __restrict__ flag) {
+  constexpr int CC = K::CC, BM = K::BM, BN = K::BN, TM = K::TM, TN = K::TN, NP = K::NP;
+  extern __shared__ __align__(16) float smem[];
+  float* sVbuf = smem;                                   // [STAGES][MAXQ][CC][BM]
+  float* sU = sVbuf + WS_STAGES * K::VSTAGE;             // [freq][CC][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(sU + (size_t)d.num_freqs * CC * BN) + 7) & ~(uintptr_t)7);
+  uint64_t* empty = full + WS_STAGES;
+
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int f0 = blockIdx.y * BN;
+  const int F = d.f;
+  const int nparts = d.n_row_parts * d.n_col_parts;
+  const int nblocks = (int)((d.tiles + BM - 1) / BM);
+
+  for (int e = tid; e < d.num_freqs * CC * BN; e += WS_THREADS) {
+    const int fl = e % BN, c = (e / BN) % CC, q = e / (BN * CC);
+    const int f = f0 + fl;
+    sU[e] = f < F ? U[((size_t)q * F + f) * CC + c] : 0.f;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < WS_STAGES; ++i) {
+      ws_bar_init(&full[i], WS_PROD);
+      ws_bar_init(&empty[i], WS_CONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp >= WS_CONS) {
+    ws_setmaxnreg_dec<WS_REG_PROD>();
+    // ================= producers: window gather + Bt.d.B -> V stage =================
+    const int ptid = tid - 32 * WS_CONS;
+    int pt[K::PPER], pch[K::PPER];
+    bool pact[K::PPER];
+#pragma unroll
+    for (int s = 0; s < K::PPER; ++s) {
+      const int e = ptid + s * 32 * WS_PROD;
+      pact[s] = e < BM * CC;
+      pt[s] = e % BM;
+      pch[s] = pact[s] ? e / BM : 0;
+    }
+    uint32_t it = 0;
+    for (int tb = blockIdx.x; tb < nblocks; tb += gridDim.x) {
+      ProdTile ptile[K::PPER];
+#pragma unroll
+      for (int s = 0; s < K::PPER; ++s) ptile[s] = prod_tile(d, x, tb * BM + pt[s], pch[s]);
+      for (int p = 0; p < nparts; ++p, ++it) {
+        const int rp = p / d.n_col_parts, cp = p % d.n_col_parts;
+        const uint32_t st = it % WS_STAGES;
+        float win[K::PPER][4][4];
+#pragma unroll
+        for (int s = 0; s < K::PPER; ++s)
+          if (pact[s]) load_window(d, ptile[s], rp, cp, win[s]);
+        ws_bar_wait(&empty[st], ((it / WS_STAGES) & 1) ^ 1);
+        float* sV = sVbuf + st * K::VSTAGE;
+#pragma unroll
+        for (int s = 0; s < K::PPER; ++s) {
+          if (!pact[s]) continue;
+#define DWM_WSTS(A, B) transform_store<K, A, B>(win[s], sV, pt[s], pch[s])
+          DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cp].count, DWM_WSTS)
+#undef DWM_WSTS
+        }
+        __syncwarp();
+        if (lane == 0) ws_bar_arrive(&full[st]);
+      }
+    }
+  } else {
+    ws_setmaxnreg_inc<WS_REG_CONS>();
+    // ================= consumers: FMA chains, At stages, register accumulators =================
+    const int tm = lane, tn = warp;
+    f2 acc[TM][NP][2][2];
+    uint32_t it = 0;
+    for (int tb = blockIdx.x; tb < nblocks; tb += gridDim.x) {
+      int qoff = 0;
+      for (int p = 0; p < nparts; ++p, ++it) {
+        const int rp = p / d.n_col_parts, cpi = p % d.n_col_parts;
+        const uint32_t st = it % WS_STAGES;
+        ws_bar_wait(&full[st], (it / WS_STAGES) & 1);
+        const float* sV = sVbuf + st * K::VSTAGE;
+        const float* sUp = sU + qoff * CC * BN;
+#define DWM_WSC(A, B) consume_part_reg<K, A, B>(sV, sUp, acc, tm, tn, p == 0)
+        DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cpi].count, DWM_WSC)
+#undef DWM_WSC
+        __syncwarp();
+        if (lane == 0) ws_bar_arrive(&empty[st]);
+        qoff += (d.row_parts[rp].count + 1) * (d.col_parts[cpi].count + 1);
+      }
+      // epilogue: 2x2 tiles -> NCHW from the accumulator registers
+      bool bad = false;
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int tile = tb * BM + tm + 32 * i;
+        if (tile >= d.tiles) continue;
+        const int tx = tile % d.tw;
+        const int t2 = tile / d.tw;
+        const int ty = t2 % d.th;
+        const int n = t2 / d.th;
+#pragma unroll
+        for (int jp = 0; jp < NP; ++jp) {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int f = f0 + tn * TN + 2 * jp + half;
+            if (f >= F) continue;
+            float* yf = y + ((size_t)n * F + f) * (size_t)d.oh * d.ow;
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) {
+              const int oy = 2 * ty + ii;
+              if (oy >= d.oh) continue;
+              const float2 a0 = upk(acc[i][jp][ii][0]);
+              const float2 a1 = upk(acc[i][jp][ii][1]);
+              const float v0 = half ? a0.y : a0.x, v1 = half ? a1.y : a1.x;
+              const int ox = 2 * tx;
+              float* dst = yf + (size_t)oy * d.ow + ox;
+              if (ox + 1 < d.ow) {
+                bad |= !(isfinite(v0) && isfinite(v1));
+                if ((d.ow & 1) == 0 && ((uintptr_t)y & 7) == 0) {
+                  __stcs(reinterpret_cast<float2*>(dst), make_float2(v0, v1));
+                } else {
+                  __stcs(dst, v0);
+                  __stcs(dst + 1, v1);
+                }
+              } else {
+                bad |= !isfinite(v0);
+                __stcs(dst, v0);
+              }
+            }
+          }
+        }
+      }
+      if (bad && flag) *flag = 1;
+    }
+  }
+}
+
+template <class K>
+int launch_ws(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
+  const size_t smem = K::smem_bytes(d.num_freqs);
+  const void* kern = (const void*)small_c_ws_kernel<K>;
+  if (int st = ensure_dynamic_smem(kern, smem)) return st;
+  int sms = 0;
+  if (int st = device_sm_count(&sms)) return st;
+  const int fblocks = (d.f + K::BN - 1) / K::BN;
+  const int64_t nblocks = (d.tiles + K::BM - 1) / K::BM;
+  int64_t gx = ((int64_t)sms + fblocks - 1) / fblocks;
+  if (gx > nblocks) gx = nblocks;
+  small_c_ws_kernel<K><<<dim3((unsigned)gx, (unsigned)fblocks), WS_THREADS, smem, s>>>(d, x, U, y, flag);
+  DWM_CUDA_TRY(cudaGetLastError());
+  return DWM_OK;
+}
+
 template <class K>
 int launch_cfg(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
   const size_t smem = K::smem_bytes(d.num_freqs);
@@ -357,6 +633,18 @@ constexpr size_t SMEM_CAP = 220 * 1024;
 // (Measured on cfg2/cfg3 against 2x4, 1x4, 1x8 with 2 CTAs/SM: see DESIGN.md.)
 template <int CC>
 int launch_cc(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
+  // warp-specialized kernel first: 64 tiles x 64 filters when F > 32, 64 x 48
+  // for F a multiple of 48 but not of 64, 32 x 64 when U is large
+  static const bool ws_off = getenv("DWM_SMALLC_LEGACY") != nullptr;
+  if (!ws_off) {
+    using W64 = WsCfg<CC, 2, 8>;
+    using W48 = WsCfg<CC, 2, 6>;
+    using T64 = WsCfg<CC, 1, 8>;
+    if (d.f % 64 != 0 && d.f % 48 == 0 && W48::smem_bytes(d.num_freqs) <= SMEM_CAP)
+      return launch_ws<W48>(d, x, U, y, flag, s);
+    if (d.f > 32 && W64::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_ws<W64>(d, x, U, y, flag, s);
+    if (d.f > 32 && T64::smem_bytes(d.num_freqs) <= SMEM_CAP) return launch_ws<T64>(d, x, U, y, flag, s);
+  }
   using Wide = Cfg<CC, 2, 8>;
   using Narrow = Cfg<CC, 4, 4>;
   using Tall = Cfg<CC, 1, 8>;
