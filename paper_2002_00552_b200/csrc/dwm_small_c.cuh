@@ -340,9 +340,12 @@ small_c_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __r
 // register budgets redistributed with setmaxnreg.  Same arithmetic in the
 // same order as small_c_kernel, so the same bits (the reference's).
 // ===========================================================================
-constexpr int WS_CONS = 8, WS_PROD = 4, WS_THREADS = 32 * (WS_CONS + WS_PROD);
+#ifndef DWM_WS_PROD
+#define DWM_WS_PROD 8  // producer warps (8: cfg2 -3 %, cfg3 -7 % vs 4, profiles/r2/ab_small_c_producers.txt)
+#endif
+constexpr int WS_CONS = 8, WS_PROD = DWM_WS_PROD, WS_THREADS = 32 * (WS_CONS + WS_PROD);
 constexpr int WS_STAGES = 3;
-constexpr int WS_REG_CONS = 208, WS_REG_PROD = 80;
+constexpr int WS_REG_CONS = 208, WS_REG_PROD = WS_PROD == 4 ? 80 : 48;  // 8 x 32 x (208 + 48) = 65536
 static_assert(WS_CONS * 32 * WS_REG_CONS + WS_PROD * 32 * WS_REG_PROD <= 65536, "register file");
 
 template <int CC_, int TM_, int TN_>
