@@ -13,6 +13,7 @@
 #include "dwm_wino.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace dwm {
@@ -213,7 +214,7 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
 // tiles, each lane one channel, so every V store is a coalesced 128-byte row
 // segment of V[fq][tile][c].  Same arithmetic (and bits) as the kernel above.
 // ---------------------------------------------------------------------------
-constexpr int IT_CB = 32;  // channels per CTA (one per lane)
+
 #ifndef DWM_IT_TROWS
 #define DWM_IT_TROWS 4  // tile rows per CTA (whole-row staging, few-frequency plans)
 #endif
@@ -260,7 +261,11 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
 #ifndef DWM_IT_MAXNREG
 #define DWM_IT_MAXNREG 56  // 5 CTAs of 224 threads per SM (tools/it_exp.sh); binary64 spills a little
 #endif
-template <typename T, bool WIDE, bool STREAM>
+// CB: channels per CTA.  32 (one per lane, every V store a 128-byte row
+// segment) or 16 (two tiles per warp step, 64-byte segments; half the staged
+// rows per CTA, so twice the resident CTAs on the stride-2 plans whose
+// staged block is large).
+template <typename T, bool WIDE, bool STREAM, int CB>
 __global__ void __maxnreg__(DWM_IT_MAXNREG)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
                             int twb_arg, int ws_arg, int trows_arg, int n0) {
@@ -270,7 +275,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   const int trows = WIDE ? 1 : trows_arg;  // tile rows per CTA (their staged rows overlap)
   const int ws = WIDE ? ws_arg : d.pad_left + d.w + d.pad_right;  // staged row width (zero-padded)
   extern __shared__ __align__(16) unsigned char it_smem_raw[];
-  T* sx = reinterpret_cast<T*>(it_smem_raw);  // [IT_CB][rows_staged][ws] with odd channel pitch
+  T* sx = reinterpret_cast<T*>(it_smem_raw);  // [CB][rows_staged][ws] with odd channel pitch
   const int pitch = rows_staged * ws + 1;
   // channel block fastest: the C/32 CTAs of one tile row (segment) run together.
   // Wide images: a CTA covers tiles [tx0, tx0 + twb) of the row and stages only
@@ -281,8 +286,8 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   const int ty0 = WIDE ? (int)(blockIdx.y / nxb) % d.th : (int)(blockIdx.y % nty) * trows;
   const int n = n0 + (WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / nty));  // image
   const int cbase = WIDE ? 2 * tx0 * d.s_w - d.pad_left : -d.pad_left;  // input column of staged column 0
-  const int c0 = blockIdx.x * IT_CB;
-  const int cb = min(IT_CB, d.c - c0);
+  const int c0 = blockIdx.x * CB;
+  const int cb = min(CB, d.c - c0);
   const int row0 = 2 * ty0 * d.s_h - d.pad_top;  // padded-input row of window sample 0 (origin 0)
 
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
@@ -341,17 +346,19 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   }
   __syncthreads();
 
+  constexpr int TPW = 32 / CB;  // tiles per warp step
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nwarps = blockDim.x / 32;
-  if (lane >= cb) return;
-  const T* sc = sx + lane * pitch;
+  const int cl = lane % CB, sub = lane / CB;
+  if (cl >= cb) return;
+  const T* sc = sx + cl * pitch;
   const int64_t tc_stride = d.tiles * d.c;
   const int tx_end = WIDE ? min(d.tw, tx0 + twb) : d.tw;
   const int ntr = min(trows, d.th - ty0);
   for (int tyl = 0; tyl < ntr; ++tyl)
-  for (int tx = tx0 + warp; tx < tx_end; tx += nwarps) {
+  for (int tx = tx0 + warp * TPW + sub; tx < tx_end; tx += nwarps * TPW) {
     const int ty = ty0 + tyl;
     const int64_t tile = ((int64_t)n * d.th + ty) * d.tw + tx;
-    T* vout = V + tile * d.c + c0 + lane;
+    T* vout = V + tile * d.c + c0 + cl;
     int fq = 0;
     // even-extension truncation only reaches an odd last tile row / column
     const bool check = 2 * ty >= d.oh - 1 || 2 * tx >= d.ow - 1;
@@ -401,6 +408,19 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   }
 }
 
+// 16-channel input-transform CTAs: only for strided plans whose 32-channel
+// staged block is large (cfg5 5x5/2: 54 KB -> 4 resident CTAs; with 16
+// channels 5: 1.58 -> 1.48 ms); every other BASELINE shape was slower
+// (cfg4 11x11 +30 %, cfg5 3x3/2 +16 %; profiles/r2/ab_it_cb16.txt).
+static bool it_prefers_cb16(const dwm_desc_t& d) {
+  if (d.s_h < 2 && d.s_w < 2) return false;
+  int rows = 0;
+  for (int i = 0; i < d.n_row_parts; ++i)
+    rows = max(rows, d.row_parts[i].origin + d.s_h * d.row_parts[i].count + 1);
+  const size_t smem32 = (size_t)32 * ((size_t)rows * (d.pad_left + d.w + d.pad_right) + 1) * sizeof(float);
+  return smem32 > 48 * 1024;
+}
+
 static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s,
@@ -424,8 +444,8 @@ int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* 
   return DWM_OK;
 }
 
-template <typename T>
-static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaStream_t s, bool* used) {
+template <typename T, int CB>
+static int launch_input_smem_cb(const dwm_desc_t& d, const void* x, void* V, cudaStream_t s, bool* used) {
   // rows a tile row reads: (largest tap origin + s*count) over row parts = r_h + s_h - 1, +1
   int rows = 0;
   for (int i = 0; i < d.n_row_parts; ++i)
@@ -438,16 +458,16 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   if (d.c < 8) return DWM_OK;
   constexpr size_t CAP = 96 * 1024;
   int twb = d.tw, ws = d.pad_left + d.w + d.pad_right;  // whole zero-padded rows
-  size_t smem = (size_t)IT_CB * ((size_t)rows * ws + 1) * sizeof(T);
+  size_t smem = (size_t)CB * ((size_t)rows * ws + 1) * sizeof(T);
   if (smem > CAP) {  // wide image: segments of the tile row, the largest multiple of 8 tiles that fits
     twb = 0;
     for (int t = 8; t < d.tw; t += 8) {
       const int w_t = 2 * d.s_w * (t - 1) + cols1;
-      if ((size_t)IT_CB * ((size_t)rows * w_t + 1) * sizeof(T) <= CAP) twb = t;
+      if ((size_t)CB * ((size_t)rows * w_t + 1) * sizeof(T) <= CAP) twb = t;
     }
     if (twb == 0) return DWM_OK;
     ws = 2 * d.s_w * (twb - 1) + cols1;
-    smem = (size_t)IT_CB * ((size_t)rows * ws + 1) * sizeof(T);
+    smem = (size_t)CB * ((size_t)rows * ws + 1) * sizeof(T);
   }
   const bool wide = twb != d.tw;
   // whole rows: stage trows tile rows per CTA when they fit (the rows
@@ -455,7 +475,7 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   int trows = 1;
   if (!wide && d.num_freqs <= IT_TROWS_MAX_FREQS) {
     const int rows_t = rows + (DWM_IT_TROWS - 1) * 2 * d.s_h;
-    const size_t smem_t = (size_t)IT_CB * ((size_t)rows_t * ws + 1) * sizeof(T);
+    const size_t smem_t = (size_t)CB * ((size_t)rows_t * ws + 1) * sizeof(T);
     if (DWM_IT_TROWS > 1 && smem_t <= CAP) {
       trows = DWM_IT_TROWS;
       rows = rows_t;
@@ -469,18 +489,20 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
   if (per_img > 65535) return DWM_OK;  // (never at BASELINE sizes) the 1-D-grid kernel takes it
   const int imgs_per_launch = 65535 / per_img;
   const bool stream = d.num_freqs > IT_STREAM_MIN_FREQS;
-  auto kern = wide ? (stream ? input_transform_smem_kernel<T, true, true> : input_transform_smem_kernel<T, true, false>)
-                   : (stream ? input_transform_smem_kernel<T, false, true> : input_transform_smem_kernel<T, false, false>);
+  auto kern = wide ? (stream ? input_transform_smem_kernel<T, true, true, CB> : input_transform_smem_kernel<T, true, false, CB>)
+                   : (stream ? input_transform_smem_kernel<T, false, true, CB> : input_transform_smem_kernel<T, false, false, CB>);
   if (int st = ensure_dynamic_smem((const void*)kern, smem)) return st;
-  // warps: a divisor of the tile count in [4, 8] so every warp gets the same number of tiles
+  // warps: a divisor of the tile-step count in [4, 8] so every warp gets the
+  // same number of tiles (a warp step covers 32 / CB tiles)
+  const int steps = (twb + 32 / CB - 1) / (32 / CB);
   int warps = 8;
-  if (twb <= 8) warps = twb;
+  if (steps <= 8) warps = steps < 1 ? 1 : steps;
   else
     for (int cand = 8; cand >= 4; --cand)
-      if (twb % cand == 0) { warps = cand; break; }
+      if (steps % cand == 0) { warps = cand; break; }
   for (int n0 = 0; n0 < d.n; n0 += imgs_per_launch) {
     const int nb = min(imgs_per_launch, d.n - n0);
-    const dim3 grid((unsigned)((d.c + IT_CB - 1) / IT_CB), (unsigned)(nb * per_img));
+    const dim3 grid((unsigned)((d.c + CB - 1) / CB), (unsigned)(nb * per_img));
     kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows, n0);
     DWM_CUDA_TRY(cudaGetLastError());
   }
@@ -490,8 +512,15 @@ static int launch_input_smem(const dwm_desc_t& d, const void* x, void* V, cudaSt
 
 int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s) {
   bool used = false;
-  const int st = dtype == DWM_F64 ? launch_input_smem<double>(d, x, V, s, &used)
-                                  : launch_input_smem<float>(d, x, V, s, &used);
+  // 16-channel CTAs: DWM_IT_CB=16 (experiments) or the rule below
+  static const int env_cb = [] {
+    const char* e = getenv("DWM_IT_CB");
+    return e ? atoi(e) : 0;
+  }();
+  const bool cb16 = env_cb ? env_cb == 16 : it_prefers_cb16(d);
+  const int st = dtype == DWM_F64 ? launch_input_smem_cb<double, 32>(d, x, V, s, &used)
+               : cb16             ? launch_input_smem_cb<float, 16>(d, x, V, s, &used)
+                                  : launch_input_smem_cb<float, 32>(d, x, V, s, &used);
   if (st || used) return st;
   const int64_t n = d.tiles * d.c;
   if (dtype == DWM_F64)

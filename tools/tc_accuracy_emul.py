@@ -15,6 +15,8 @@ Schemes:
   split<K>  main (hi*hi) accumulator per K channels, one correction
             accumulator over all channels; mq = sum(main chunks) + corr
   long      one accumulator over all channels (corr first per 32 ch)
+  <scheme>_tv  V's hi operand is raw V truncated by the tensor core (SS-mode A
+            straight from the TMA stage) instead of the RN split
   pair<S>   main (hi*hi) and correction (hi*lo + lo*hi) in two accumulators,
             both fresh per S channels (one N=128 MMA [Uh;Ul] + one N=64
             MMA Vl*Uh per K step); chunk = main + corr, chunks summed in FP32
@@ -60,7 +62,12 @@ def step(acc, a, b, first):
 
 def contraction(V, U, scheme):
     Q, T, C = V.shape
-    vh = rna_tf32(V)
+    if scheme.endswith("_tv"):
+        # raw V as the hi operand (the tensor core truncates it to TF32); lo = V - trunc(V)
+        scheme = scheme[:-3]
+        vh = trunc_tf32(V)
+    else:
+        vh = rna_tf32(V)
     vl = trunc_tf32((V - vh).astype(np.float32))
     uh = rna_tf32(U)
     ul = rna_tf32((U - uh).astype(np.float32))
