@@ -334,6 +334,9 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
     independent, so chunking changes no result bit).  Runs with ``s`` current."""
     torch = _torch()
     n = x_h.shape[0]
+    # 8 chunks: the first H2D / last D2H chunk is exposed (1/8 of the
+    # transfer); 16 measured slower on cfg4 11x11 (32-image chunks fill 1.3
+    # waves of the persistent GEMM: 18.0k vs 20.2k images/s end to end)
     chunks = 1 if n < 2 else min(8, n)
     bounds = [round(i * n / chunks) for i in range(chunks + 1)]
     x_d = torch.empty(x_h.shape, dtype=x_h.dtype, device=dev)
@@ -341,23 +344,31 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
     s_in, s_out = _side_streams(dev)
     s_in.wait_stream(s)
     s_out.wait_stream(s)
-    ws_bytes = max(lib.dwm_workspace_bytes(_native.make_desc(
-        b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad), code, algo_code)
-        for b0, b1 in zip(bounds, bounds[1:]))
+    descs = [_native.make_desc(b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad)
+             for b0, b1 in zip(bounds, bounds[1:])]
+    # one engine and one filter transform for all chunks (the engine choice
+    # does not depend on the batch; resolve it once so U's layout matches)
+    sel = lib.dwm_select_algo(descs[0], code, algo_code)
+    if sel < 0:
+        _native.check(lib.dwm_conv2d_forward(descs[0], code, algo_code, None, None, None, None, 0, None,
+                                             s.cuda_stream), "dwm_conv2d_forward")
+    u = _workspace(lib.dwm_filter_bytes(descs[0], code, sel), dev)
+    _native.check(lib.dwm_prepare_filter(descs[0], code, sel, w_d.data_ptr(), u.data_ptr(), s.cuda_stream),
+                  "dwm_prepare_filter")
+    ws_bytes = max(lib.dwm_workspace_bytes(dk, code, sel) for dk in descs)
     ws = _workspace(ws_bytes, dev)
-    for b0, b1 in zip(bounds, bounds[1:]):
+    for (b0, b1), dk in zip(zip(bounds, bounds[1:]), descs):
         with torch.cuda.stream(s_in):
             x_d[b0:b1].copy_(x_h[b0:b1], non_blocking=True)
             ev_in = torch.cuda.Event()
             ev_in.record(s_in)
         s.wait_event(ev_in)
-        dk = _native.make_desc(b1 - b0, desc.c, desc.h, desc.w, desc.f, spec.kernel, spec.stride, spec.pad)
         # chunk bases need only natural alignment (the kernels take their
         # vector paths only on 16-/8-byte aligned bases)
-        st = lib.dwm_conv2d_forward(dk, code, algo_code, x_d[b0].data_ptr(), w_d.data_ptr(),
-                                    y_d[b0].data_ptr(), ws.data_ptr(), ws_bytes,
-                                    flag.data_ptr() if flag is not None else None, s.cuda_stream)
-        _native.check(st, "dwm_conv2d_forward")
+        st = lib.dwm_conv2d_forward_prepared(dk, code, sel, x_d[b0].data_ptr(), u.data_ptr(),
+                                             y_d[b0].data_ptr(), ws.data_ptr(), ws_bytes,
+                                             flag.data_ptr() if flag is not None else None, s.cuda_stream)
+        _native.check(st, "dwm_conv2d_forward_prepared")
         ev_done = torch.cuda.Event()
         ev_done.record(s)
         s_out.wait_event(ev_done)
