@@ -261,10 +261,27 @@ def reference_impl():
 
 
 def cpu_threads():
-    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
-        if os.environ.get(var):
-            return int(os.environ[var])
+    """BLAS threads the CPU reference runs with: every host core.  (torchrun
+    sets OMP_NUM_THREADS=1 for multi-rank jobs; the reference arm raises the
+    BLAS pool back to all cores with threadpoolctl, see all_cores().)"""
     return os.cpu_count()
+
+
+class all_cores:
+    """Context: BLAS thread pools at os.cpu_count() threads (the reference's
+    NumPy/OpenBLAS path uses all host cores, whatever OMP_NUM_THREADS says)."""
+
+    def __enter__(self):
+        try:
+            from threadpoolctl import threadpool_limits
+            self._ctl = threadpool_limits(limits=os.cpu_count(), user_api="blas")
+        except Exception:  # threadpoolctl missing: run with the process default
+            self._ctl = None
+        return self
+
+    def __exit__(self, *exc):
+        if self._ctl is not None:
+            self._ctl.restore_original_limits()
 
 
 def cpu_model():
@@ -286,6 +303,11 @@ def cpu_reference_rate(wl, seconds: float):
     w = rng.standard_normal((wl.c_out, wl.c_in, wl.kernel, wl.kernel)).astype(np.float32)
     rates = {}
     t_end = time.perf_counter() + seconds
+    with all_cores():
+        return _cpu_rates(fn, spec, w, rng, wl, seconds, t_end, rates), kind, what
+
+
+def _cpu_rates(fn, spec, w, rng, wl, seconds, t_end, rates):
     for n in (1, 2):
         x = rng.standard_normal((n, wl.c_in, wl.hw, wl.hw)).astype(np.float32)
         fn(x, w, spec)  # warm (BLAS threads, page-in)
@@ -300,7 +322,7 @@ def cpu_reference_rate(wl, seconds: float):
             if n == 1 and time.perf_counter() > t_end - seconds / 2:
                 break
         rates[n] = n / best
-    return rates, kind, what
+    return rates
 
 
 def run_reference_arm(args, wl, rank, world):
@@ -313,13 +335,14 @@ def run_reference_arm(args, wl, rank, world):
     rng = np.random.default_rng(0)
     x = rng.standard_normal((images, wl.c_in, wl.hw, wl.hw)).astype(np.float32)
     w = rng.standard_normal((wl.c_out, wl.c_in, wl.kernel, wl.kernel)).astype(np.float32)
-    for _ in range(args.warmup):
-        fn(x, w, spec)
     times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        fn(x, w, spec)
-        times.append(time.perf_counter() - t0)
+    with all_cores():
+        for _ in range(args.warmup):
+            fn(x, w, spec)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            fn(x, w, spec)
+            times.append(time.perf_counter() - t0)
     total = sum(times)
     value = images * args.steps / total
     cores = cpu_threads()
