@@ -77,13 +77,17 @@ class DWMConvGraph:
             dst.copy_(src, non_blocking=True)
 
     def __call__(self, x, w, out=None):
-        self._copy_in(self.x, x)
-        self._copy_in(self.w, w)
-        self.graph.replay()
-        y = self.y
-        if out is not None:
-            out.copy_(y, non_blocking=True)
-            y = out
-        if self.check_finite and int(self.flag.item()) != 0:
-            raise FloatingPointError("dwm_conv2d produced non-finite values")
+        """Replay on the current stream of the graph's device.  With
+        ``check_finite=False`` nothing synchronizes: the result (and a host
+        ``out``) is ready once that stream is."""
+        with torch.cuda.device(self.device):
+            self._copy_in(self.x, x)
+            self._copy_in(self.w, w)
+            self.graph.replay()
+            y = self.y
+            if out is not None:
+                out.copy_(y, non_blocking=True)
+                y = out
+            if self.check_finite and int(self.flag.item()) != 0:
+                raise FloatingPointError("dwm_conv2d produced non-finite values")
         return y
