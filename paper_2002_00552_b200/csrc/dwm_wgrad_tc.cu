@@ -198,8 +198,11 @@ wgrad_tc_kernel(const dwm_desc_t d, int64_t t_pad, const __grid_constant__ CUten
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.acc_empty[ab]);
+        // +1 ulp away from zero: the 4 main-product steps of the chunk each
+        // truncate toward zero (dwm_gemm_tc.cu trunc_compensate; an integer
+        // add on the float bits)
 #pragma unroll
-        for (int j = 0; j < EC; ++j) mid[j] = __fadd_rn(mid[j], part[j]);
+        for (int j = 0; j < EC; ++j) mid[j] = __fadd_rn(mid[j], __uint_as_float(__float_as_uint(part[j]) + 1u));
         if (++nb == BLOCK_CHUNKS) {
           nb = 0;
 #pragma unroll

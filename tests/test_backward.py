@@ -6,7 +6,8 @@ and against the binary64 analytic oracle.
 Tolerances (written here):
   * binary64: max |gpu - oracle| <= 1e-10 (the reference's own criterion,
     test_engines_backward.py:96-97) and max |gpu - reference dwm64| <= 1e-10.
-  * binary32: MSE vs the binary64 oracle <= 4 x the reference's binary32 MSE
+  * binary32: MSE vs the binary64 oracle <= the reference's binary32 MSE
+    (<= 4x for gradients with fewer than 4096 entries, where the ratio is noise)
     (plus 1e-14 absolute for the all-but-exact tiny cases) -- the B200 data
     gradient runs the forward engine on the adjoint problem and the weight
     gradient is a different (fixed) summation order, so bits differ but the
@@ -114,6 +115,19 @@ def _tc_wgrad_ok(case):
     return c % 32 == 0 and c >= 64 and f >= 64
 
 
+def _record(key, value):
+    """Achieved error ratios vs the reference, appended to $DWM_RATIO_OUT."""
+    import json
+    import os
+    out = os.environ.get("DWM_RATIO_OUT")
+    if not out:
+        return
+    old = json.loads(open(out).read()) if os.path.exists(out) else {}
+    old[key] = value
+    with open(out, "w") as fh:
+        json.dump(old, fh, indent=1, sort_keys=True)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("wgrad", ["exact", "tc"])
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
@@ -126,8 +140,14 @@ def test_backward_f32_error_at_reference_level(cuda, case, wgrad):
     assert gd.dtype == np.float32 and gw.dtype == np.float32
     k = case["name"]
     want_d, want_w = ARR[f"{k}/gd64"], ARR[f"{k}/gw64"]
-    assert mse(gd, want_d) <= 4 * case["ref_mse_gd32"] + 1e-14
-    assert mse(gw, want_w) <= 4 * case["ref_mse_gw32"] + 1e-14
+    rd, rw = mse(gd, want_d) / max(case["ref_mse_gd32"], 1e-300), mse(gw, want_w) / max(case["ref_mse_gw32"], 1e-300)
+    _record(f"backward_f32/{k}/{wgrad}", {"data": rd, "weights": rw, "outputs": [int(gd.size), int(gw.size)]})
+    # at or below the reference's binary32 error; with fewer than 4096 outputs
+    # the MSE ratio is sampling noise (0.2-2.7x observed), 4x slack there
+    slack_d = 1.0 if gd.size >= 4096 else 4.0
+    slack_w = 1.0 if gw.size >= 4096 else 4.0
+    assert mse(gd, want_d) <= slack_d * case["ref_mse_gd32"] + 1e-14, rd
+    assert mse(gw, want_w) <= slack_w * case["ref_mse_gw32"] + 1e-14, rw
 
 
 @pytest.mark.gpu
