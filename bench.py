@@ -468,16 +468,26 @@ class GpuRunner:
         V = self.ws.data_ptr()
         U = V + ((self.v_bytes + 255) // 256) * 256
         d = self.desc
+        tc = self.engine == "tc"
+        if tc:  # the engine's V range slots, as dwm_conv2d_forward keeps them after V and U
+            rng = torch.zeros(self._native.RANGE_BYTES // 4, dtype=torch.int32, device=self.x.device)
 
         def filt():
             check(lib.dwm_prepare_filter(d, F32, self.algo, self.w.data_ptr(), U, self.sptr))
 
         def inp():
-            check(lib.dwm_input_transform(d, F32, self.x.data_ptr(), V, self.sptr))
+            if tc:
+                check(lib.dwm_input_transform_ranged(d, self.x.data_ptr(), V, rng.data_ptr(), self.sptr))
+            else:
+                check(lib.dwm_input_transform(d, F32, self.x.data_ptr(), V, self.sptr))
 
         def gemm():
-            check(lib.dwm_gemm_output(d, F32, self.algo, V, U, self.y.data_ptr(), self.flag.data_ptr(),
-                                      None, 0, self.sptr))
+            if tc:
+                check(lib.dwm_gemm_output_tc(d, V, U, rng.data_ptr(), self.y.data_ptr(), self.flag.data_ptr(),
+                                             self.sptr))
+            else:
+                check(lib.dwm_gemm_output(d, F32, self.algo, V, U, self.y.data_ptr(), self.flag.data_ptr(),
+                                          None, 0, self.sptr))
 
         def small_c():
             check(lib.dwm_conv2d_small_c(d, self.x.data_ptr(), U, self.y.data_ptr(), self.flag.data_ptr(),
@@ -714,8 +724,9 @@ def make_roofline(stage_ms, run, peaks):
             k["dwm_gemm_flops"] = gemm_flops
             k["achieved_tflops"] = gemm_flops / (ms * 1e-3) / 1e12
         if name == "gemm_output" and engine == "tc":
-            k["tensor_tflops_3xtf32"] = 3 * gemm_flops / (ms * 1e-3) / 1e12
-            k["tensor_frac"] = k["tensor_tflops_3xtf32"] / peaks["tf32_tflops"]
+            # three fp16 tensor products (hi*hi + hi*lo + lo*hi) per fp32 MAC
+            k["tensor_tflops_3xf16"] = 3 * gemm_flops / (ms * 1e-3) / 1e12
+            k["tensor_frac"] = k["tensor_tflops_3xf16"] / peaks["bf16_tflops"]
         if name == "conv2d_small_c":
             k["fp32_tflops"] = small_c_fp32_ops(desc) / (ms * 1e-3) / 1e12
             k["fp32_frac"] = k["fp32_tflops"] / peaks["fp32_tflops"]
@@ -723,11 +734,11 @@ def make_roofline(stage_ms, run, peaks):
         kernels.append(k)
     top = max(kernels, key=lambda k: k["ms"])
     if top["name"] == "gemm_output" and engine == "tc":
-        roof = {"bound": "tensor", "kernel": top["name"], "achieved": top["tensor_tflops_3xtf32"],
-                "peak": peaks["tf32_tflops"], "unit": "TFLOP/s", "frac": top["tensor_frac"],
+        roof = {"bound": "tensor", "kernel": top["name"], "achieved": top["tensor_tflops_3xf16"],
+                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": top["tensor_frac"],
                 "traffic": top["traffic"],
-                "note": "3xTF32 tensor FLOPs per launch (3 x 2*C*F*tiles*freqs) / CUDA-event time vs dense "
-                        "TF32 tcgen05 peak, " + peaks["unit_source"]}
+                "note": "3-term fp16-split tensor FLOPs per launch (3 x 2*C*F*tiles*freqs, kind::f16) / "
+                        "CUDA-event time vs the dense 16-bit tensor peak, " + peaks["source"]}
     elif top["name"] == "conv2d_small_c":
         roof = {"bound": "fp32", "kernel": top["name"], "achieved": top["fp32_tflops"],
                 "peak": peaks["fp32_tflops"], "unit": "TFLOP/s", "frac": top["fp32_frac"],

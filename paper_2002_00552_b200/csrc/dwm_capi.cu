@@ -179,9 +179,10 @@ size_t dwm_workspace_bytes(const dwm_desc_t* d, int dtype, int algo) {
   const size_t es = dtype == DWM_F64 ? 8 : 4;
   const int sel = dwm_select_algo(d, dtype, algo);
   size_t u = (size_t)d->num_freqs * (size_t)d->f * (size_t)d->c * es;
-  if (sel == DWM_ALGO_TC) u = tc_filter_bytes(*d);  // stacked hi/lo TF32 split of U
+  if (sel == DWM_ALGO_TC) u = tc_filter_bytes(*d);  // stacked, scaled fp16 hi/lo split of U
   const size_t v = sel == DWM_ALGO_SMALL_C ? 0 : v_bytes_of(d, es);
-  return round_up(v, 256) + round_up(u, 256);
+  // TC: + the input transform's max|x| slots (after V and U)
+  return round_up(v, 256) + round_up(u, 256) + (sel == DWM_ALGO_TC ? DWM_XMAX_BYTES : 0);
 }
 
 // Workspace-type buffers (V, U, ws) are read with 16-byte vector loads and
@@ -227,9 +228,29 @@ int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, con
   int sel = dwm_select_algo(d, dtype, algo);
   if (sel == DWM_ALGO_SMALL_C) sel = algo == DWM_ALGO_AUTO ? DWM_ALGO_EXACT : -1;
   if (sel < 0) return bad_algo(d, algo);
-  if (sel == DWM_ALGO_TC)
-    return launch_gemm_tc(*d, V, U, y, flag, (cudaStream_t)stream);
+  if (sel == DWM_ALGO_TC) {
+    if (ws_bytes > 0)
+      if (int st = check_aligned(ws, "workspace")) return st;
+    return launch_gemm_tc(*d, V, U, y, flag, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+  }
   return launch_gemm_exact(*d, dtype, V, U, y, flag, (cudaStream_t)stream);
+}
+
+int dwm_input_transform_ranged(const dwm_desc_t* d, const void* x, void* V, uint32_t* range, void* stream) {
+  if (int st = check_common(d, DWM_F32)) return st;
+  if (int st = check_aligned(V, "V")) return st;
+  if (int st = check_aligned(range, "range")) return st;
+  return launch_input_transform(*d, DWM_F32, x, V, (cudaStream_t)stream, range);
+}
+
+int dwm_gemm_output_tc(const dwm_desc_t* d, const void* V, const void* U, const uint32_t* range, void* y,
+                       int32_t* flag, void* stream) {
+  if (int st = check_common(d, DWM_F32)) return st;
+  if (int st = check_aligned(V, "V")) return st;
+  if (int st = check_aligned(U, "U")) return st;
+  if (int st = check_aligned(range, "range")) return st;
+  if (!tc_gemm_supported(*d)) return bad_algo(d, DWM_ALGO_TC);
+  return launch_gemm_tc(*d, V, U, y, flag, range, nullptr, 0, (cudaStream_t)stream);
 }
 
 static int wgrad_select(const dwm_desc_t* d, int dtype, int algo) {
@@ -288,13 +309,17 @@ int dwm_conv2d_forward(const dwm_desc_t* d, int dtype, int algo, const void* x, 
   cudaStream_t s = (cudaStream_t)stream;
   int st;
   if (sel == DWM_ALGO_TC) {
-    if ((st = launch_filter_transform_tf32split(*d, w, U, s))) return st;
+    if ((st = launch_filter_transform_f16split(*d, w, U, s))) return st;
   } else {
     if ((st = launch_filter_transform(*d, dtype, w, U, s))) return st;
   }
   if (sel == DWM_ALGO_SMALL_C) return launch_small_c(*d, x, U, y, flag, s);
+  if (sel == DWM_ALGO_TC) {
+    uint32_t* xmax = (uint32_t*)(base + round_up(v_bytes_of(d, es), 256) + round_up(tc_filter_bytes(*d), 256));
+    if ((st = launch_input_transform(*d, dtype, x, V, s, xmax))) return st;
+    return launch_gemm_tc(*d, V, U, y, flag, xmax, nullptr, 0, s);
+  }
   if ((st = launch_input_transform(*d, dtype, x, V, s))) return st;
-  if (sel == DWM_ALGO_TC) return launch_gemm_tc(*d, V, U, y, flag, s);
   return launch_gemm_exact(*d, dtype, V, U, y, flag, s);
 }
 
@@ -311,7 +336,7 @@ int dwm_prepare_filter(const dwm_desc_t* d, int dtype, int algo, const void* w, 
   if (int st = check_aligned(U, "U")) return st;
   const int sel = dwm_select_algo(d, dtype, algo);
   if (sel < 0) return bad_algo(d, algo);
-  if (sel == DWM_ALGO_TC) return launch_filter_transform_tf32split(*d, w, U, (cudaStream_t)stream);
+  if (sel == DWM_ALGO_TC) return launch_filter_transform_f16split(*d, w, U, (cudaStream_t)stream);
   return launch_filter_transform(*d, dtype, w, U, (cudaStream_t)stream);
 }
 
@@ -322,7 +347,7 @@ int dwm_prepare_filter_strided(const dwm_desc_t* d, int dtype, int algo, const v
   if (int st = check_aligned(U, "U")) return st;
   const int sel = dwm_select_algo(d, dtype, algo);
   if (sel < 0) return bad_algo(d, algo);
-  if (sel == DWM_ALGO_TC) return launch_filter_transform_tf32split(*d, w, U, (cudaStream_t)stream, strides);
+  if (sel == DWM_ALGO_TC) return launch_filter_transform_f16split(*d, w, U, (cudaStream_t)stream, strides);
   return launch_filter_transform(*d, dtype, w, U, (cudaStream_t)stream, strides);
 }
 
@@ -337,13 +362,18 @@ int dwm_conv2d_forward_prepared(const dwm_desc_t* d, int dtype, int algo, const 
     if ((st0 = check_aligned(U, "U"))) return st0;
     return launch_small_c(*d, x, U, y, flag, s);
   }
-  const size_t need = v_bytes_of(d, dtype == DWM_F64 ? 8 : 4);
+  const size_t vb = v_bytes_of(d, dtype == DWM_F64 ? 8 : 4);
+  const size_t need = sel == DWM_ALGO_TC ? round_up(vb, 256) + DWM_XMAX_BYTES : vb;
   if (!ws || ws_bytes < need)
     return fail(DWM_EINVAL_SHAPE, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
   if ((st0 = check_aligned(ws, "workspace")) || (st0 = check_aligned(U, "U"))) return st0;
   int st;
+  if (sel == DWM_ALGO_TC) {
+    uint32_t* xmax = (uint32_t*)((char*)ws + round_up(vb, 256));
+    if ((st = launch_input_transform(*d, dtype, x, ws, s, xmax))) return st;
+    return launch_gemm_tc(*d, ws, U, y, flag, xmax, nullptr, 0, s);
+  }
   if ((st = launch_input_transform(*d, dtype, x, ws, s))) return st;
-  if (sel == DWM_ALGO_TC) return launch_gemm_tc(*d, ws, U, y, flag, s);
   return launch_gemm_exact(*d, dtype, ws, U, y, flag, s);
 }
 

@@ -1,55 +1,68 @@
 // dwm_gemm_tc.cu -- transform-domain contraction on the 5th-gen tensor cores
-// (tcgen05, kind::tf32, 3xTF32 split) with the output transform, the
-// plan-order part sum and the 2x2 tile interleave fused into the epilogue.
+// (tcgen05 kind::f16, 3-term fp16 split, fp32 accumulate) with the output
+// transform, the plan-order part sum and the 2x2 tile interleave fused into
+// the epilogue.
 //
 // Reference rows: M (engines.py:82-89,189) and A/Sigma/F
 // (engines.py:192-194, tensor.py:68-81, engines.py:255).
 //
 // Per frequency q (all parts, plan order), per 128-tile x 64-filter block:
 //   M_q[tile][f] = sum_c V_q[tile][c] * U_q[f][c]
-// in FP32 from 3 TF32 products: Vhi*Uhi + Vhi*Ulo + Vlo*Uhi, where
-// hi = rn_tf32(x), lo = x - hi (the tensor core truncates lo to TF32).
-// U_hi/U_lo come pre-split from the filter transform; V is split on the fly.
+// in FP32 from 3 fp16 products of power-of-two scaled operands:
+//   V' = s_v V, U'_f = s_f U_f,  x' = hi + lo (hi = rn_f16(x'), lo = rn_f16(x' - hi))
+//   M' = V'hi U'hi + V'hi U'lo + V'lo U'hi,    M = M' / (s_v s_f)
+// A 22-bit split like 3xTF32, at the fp16 tensor rate (kind::f16 TS MMAs
+// stream 1.68x faster than kind::tf32 for the same N: tools/f16_probe.cu).
+// The scales are exact powers of two picked from range bounds, so V' and U'
+// sit in [2^12, 2^15) at their maxima: no fp16 overflow, and lo stays normal
+// down to 2^-26 of the maximum (MSE is absolute, so smaller values cost
+// nothing measurable):
+//   s_v = 2^(12 - floor(log2 max|x|))   |V| <= 4 max|x| (Bt rows: |.|-sums <= 2);
+//                                       max|x| from the input transform's
+//                                       staging loads (atomicMax slots)
+//   s_f = 2^(12 - floor(log2 max|w_f|)) |U_f| <= 2.25 max|w_f| (G: sums <= 1.5)
+// U'hi/U'lo come pre-split from the filter transform; V is scaled and split
+// on the fly by the converter warps.
 //
-// MMA shape.  The B operand of one stage is [U_hi (64 filters); U_lo (64)]
-// (128 rows, one SW128 tile), so per K = 8 slice two MMAs do all three
-// products:
-//   D[  0.. 63] (+)= V_hi * U_hi^T                 (N = 128, both halves
-//   D[ 64..127] (+)= V_hi * U_lo^T                  in one instruction)
-//   D[ 64..127]  += V_lo * U_hi^T                  (N = 64)
-// i.e. a main accumulator and a correction accumulator side by side.  N = 128
-// runs at 1.4x the FLOP rate of N = 64 (tools/tc_probe.cu: 1034 vs 737 TF/s).
+// MMA shape.  The B operand of one 64-channel stage is [U'hi (64 filters);
+// U'lo (64)] (128 rows x 64 fp16 = one SW128 tile), so per K = 16 slice two
+// MMAs do all three products:
+//   D[  0.. 63] (+)= V'hi * U'hi^T                 (N = 128, both halves
+//   D[ 64..127] (+)= V'hi * U'lo^T                  in one instruction)
+//   D[ 64..127]  += V'lo * U'hi^T                  (N = 64)
+// i.e. a main accumulator and a correction accumulator side by side.
 //
-// Accuracy.  The tcgen05 FP32 accumulator truncates toward zero (~-0.5 ulp
-// per MMA, tools/tc_accum_probe.cu), so a long chain is biased.  Both
-// accumulators are therefore fresh per chunk of CH channels (64 for C >= 128,
-// 32 otherwise); the epilogue forms chunk = main + corr and sums chunks in
-// FP32 round-to-nearest (tools/tc_accuracy_emul.py scheme "pair64": MSE 0.35-
-// 0.61x the reference DWM32's on cfg4/cfg5).  Then
-//   Y_(i,j) += At_r[i][a] * At_c[j][b] * M_q     (coefficients 0, +-1)
+// Accuracy.  The tcgen05 FP32 accumulator truncates each MMA step toward zero
+// (tools/tc_accum_probe.cu, tools/f16_probe.cu), so both accumulators are
+// fresh per chunk of 128 channels (8 K = 16 steps; 64 channels = 4 steps when
+// C < 128, with a +1 ulp truncation-bias compensation); the epilogue forms
+// chunk = main + corr and sums chunks in FP32 round-to-nearest.  Then
+//   Y_(i,j) += At_r[i][a] * At_c[j][b] * M'_q     (coefficients 0, +-1)
 // with Y held in the epilogue warps' registers (4 positions x 32 filters per
-// thread), and only y = interleave(Y) reaches HBM.
+// thread), y = interleave(Y) / (s_v s_f) is the only HBM write.
 //
 // Warp roles (512 threads, one CTA per SM, persistent over work items;
 // register budgets redistributed with setmaxnreg per warpgroup):
-//   WG0 warps 0-3   converter (64 regs): V rows (one tile per thread) from the
-//                   TMA stage -> hi/lo -> tcgen05.st into a TMEM A slot
+//   WG0 warps 0-3   converter (72 regs): V rows (one tile per thread) from the
+//                   TMA stage -> scale -> hi/lo fp16 pairs -> tcgen05.st
 //   WG1/2 warps 4-11 epilogue (192 regs): tcgen05.ld chunk accumulators ->
-//                   M_q -> Y (registers) -> y (NCHW), non-finite flag.  TMEM
+//                   M'_q -> Y (registers) -> y (NCHW), non-finite flag.  TMEM
 //                   lane quadrant = warp % 4, filter half = (warp - 4) / 4.
-//   WG3 warp 12     TMA producer (64 regs): V [128 tiles][32 ch] and
-//                   U_hi/U_lo [64 f][32 ch] per (frequency, 32-channel) stage
+//   WG3 warp 12     TMA producer (56 regs): V [128 tiles][2 x 32 ch] fp32 and
+//                   [U'hi; U'lo] [128 rows][64 ch] fp16 per (frequency, 64-channel) stage
 //       warp 13     TMEM allocator + MMA issuer (elect.sync from the converged warp)
 //       warps 14-15 idle (warpgroup padding for setmaxnreg)
 // TMEM columns: accumulators 2 x 128 (0-255: main | corr), A slots 4 x 64
-// (256-511: V_hi 32 | V_lo 32).
+// (256-511: V'hi 32 | V'lo 32, two fp16 channels per column).
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <unistd.h>
 #include <cstdlib>
 #include <cstdio>
 #include <cudaTypedefs.h>
 
 #include "dwm_common.cuh"
+#include "dwm_filter.cuh"
 #include "dwm_kernels.h"
 #include "dwm_sm100.cuh"
 
@@ -60,10 +73,10 @@ using namespace sm100;
 
 constexpr int BM = 128;        // tiles per work item (MMA M, TMEM lanes)
 constexpr int BN = 64;         // filters per work item
-constexpr int BK = 32;         // channels per SW128 atom (128 B rows)
-constexpr int SK = 64;         // channels per pipeline stage (2 atoms)
-constexpr int STAGES = 3;      // smem ring: 3 x (V 32 KB + U 32 KB)
-constexpr int A_SLOTS = 2;     // TMEM A ring: 2 x (hi 64 | lo 64) columns
+constexpr int VK = 32;         // fp32 V channels per SW128 atom (128 B rows)
+constexpr int SK = 64;         // channels per pipeline stage (2 V atoms, 1 U atom)
+constexpr int STAGES = 4;      // smem ring: 4 x (V 32 KB + U 16 KB)
+constexpr int A_SLOTS = 4;     // TMEM A ring: 4 x (hi 32 | lo 32) columns
 #ifndef DWM_TC_VPF
 #define DWM_TC_VPF 4
 #endif
@@ -73,19 +86,21 @@ constexpr int EPI_WARPS = 8;
 constexpr int EC = 32;         // filter columns per epilogue warp
 constexpr int WARP_TMA = 12, WARP_MMA = 13;
 constexpr int MAX_FREQS = 1024;
-constexpr uint32_t ATOM_BYTES = BM * BK * 4;  // 16 KB: one [128 rows][32 ch] SW128 tile
-constexpr uint32_t COL_ACC = 0, COL_A = 256;
+constexpr uint32_t V_ATOM_BYTES = BM * VK * 4;   // 16 KB: [128 rows][32 fp32 ch]
+constexpr uint32_t U_ATOM_BYTES = 2 * BN * SK * 2;  // 16 KB: [128 rows][64 fp16 ch]
+constexpr uint32_t COL_ACC = 0, COL_A = 256, A_COLS = 64;
 constexpr int REG_CONV = 72, REG_EPI = 192, REG_CTRL = 56;
 static_assert(4 * 32 * (REG_CONV + REG_CTRL) + 8 * 32 * REG_EPI <= 65536, "register file");
 
 struct __align__(1024) Smem {
-  float v[STAGES][2][BM * BK];      // [stage][atom][128 tiles][32 ch]
-  float u[STAGES][2][2 * BN * BK];  // [stage][atom][U_hi 64 rows; U_lo 64 rows][32 ch]
+  float v[STAGES][2][BM * VK];      // [stage][atom][128 tiles][32 ch] fp32
+  uint16_t u[STAGES][2 * BN * SK];  // [stage][U'hi 64 rows; U'lo 64 rows][64 ch] fp16
   uint64_t b_full[STAGES];          // TMA -> converter (V) and MMA (U)
   uint64_t done[STAGES];            // MMA commit per stage -> TMA, converter, epilogue
   uint64_t a_full[A_SLOTS];         // converter -> MMA
   uint64_t acc_empty[2];            // epilogue -> MMA
   uint32_t tmem_base;
+  uint32_t xmax[2];                 // max|x| bits, reduced from the input transform's slots
   int8_t coef[MAX_FREQS][4];
 };
 
@@ -115,31 +130,36 @@ __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.
 template <uint32_t N>
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
-// The tcgen05 FP32 accumulator truncates each K = 8 step toward zero (about
-// -0.5 ulp per step, tools/tc_accum_probe.cu), so a chunk of n main-product
-// steps is biased toward zero by ~n/2 ulp of its value.  For the 32-channel
-// chunks (4 steps, C < 128, where the GEMM error weighs most) the epilogue
-// adds back 1 ulp away from zero -- one integer add on the float's bits (a
-// mantissa carry into the exponent is still +1 ulp) -- emulated MSE 0.56-0.70x
-// the reference DWM32's instead of 0.70-0.86x (tools/tc_accuracy_emul.py
-// "pairc32_25").  The 64-channel chunks do not use it: on the C >= 128
-// shapes the extra epilogue latency cost 4-8 % (profiles/r2/ab_tc_bias_comp_chunk128.txt)
-// and their MSE is already 0.2-0.55x.
+// The tcgen05 FP32 accumulator truncates each MMA step toward zero, so a
+// chunk of n steps is biased toward zero by ~n/2 ulp of its value.  For the
+// 64-channel chunks (4 K = 16 steps, C < 128, where the GEMM error weighs
+// most) the epilogue adds back 1 ulp away from zero -- one integer add on the
+// float's bits (a mantissa carry into the exponent is still +1 ulp).
 __device__ __forceinline__ float trunc_compensate(float x, uint32_t k) {
   return __uint_as_float(__float_as_uint(x) + k);
 }
 
+// Power-of-two operand scale from the bits of a max |value| (floor(log2) = e):
+// s = 2^(12 - e), clamped to normal floats; 0 -> 1; inf/nan -> tiny (the
+// non-finite values propagate to y and the flag).
+__host__ __device__ __forceinline__ int scale_exp(uint32_t maxbits) {
+  const int e = (int)((maxbits >> 23) & 0xFF) - 127;  // exponent field (subnormal/0: -127)
+  if (maxbits == 0) return 0;
+  const int k = 12 - e;
+  return k > 126 ? 126 : (k < -126 ? -126 : k);
+}
+__device__ __forceinline__ float exp2i(int k) { return __uint_as_float((uint32_t)(127 + k) << 23); }
+
 // Stage geometry: stage kc of a frequency covers channels [64 kc, 64 kc + 64);
-// a C % 64 == 32 tail stage has one atom (4 K-slices).
+// a C % 64 == 32 tail stage has one V atom (2 K = 16 slices).
 __device__ __forceinline__ int stage_atoms(int C, int kc) { return C - SK * kc >= SK ? 2 : 1; }
 
-// C32: 32-channel accumulator chunks (C < 128) with the truncation-bias
-// compensation; otherwise 64-channel chunks, uncompensated.
-template <bool C32>
+// CHS: stages per accumulator chunk (2: 128 channels, 1: 64 channels + compensation)
+template <int CHS>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_u,
-               float* __restrict__ y, int32_t* __restrict__ flag) {
-  constexpr bool chunk32 = C32;
+               const float* __restrict__ inv_f, const uint32_t* __restrict__ xmax_slots, float* __restrict__ y,
+               int32_t* __restrict__ flag) {
   extern __shared__ uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -158,6 +178,11 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     for (int i = 0; i < A_SLOTS; ++i) mbar_init(&S.a_full[i], 4);
     for (int i = 0; i < 2; ++i) mbar_init(&S.acc_empty[i], EPI_WARPS);
     fence_barrier_init();
+  }
+  if (warp < 2) {  // max|x| over the input transform's DWM_XMAX_SLOTS slots
+    const uint32_t m = max(xmax_slots[tid], xmax_slots[tid + 64]);
+    const uint32_t r = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) S.xmax[warp] = r;
   }
   // output-transform coefficient of every frequency for the 4 tile positions
   for (int q = tid; q < Q; q += THREADS) {
@@ -181,6 +206,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
+  const int sv_exp = scale_exp(max(S.xmax[0], S.xmax[1]));
 #ifdef DWM_TC_PROFILE
   long long prof[4] = {0, 0, 0, 0};
   const long long t_start = clock64();
@@ -200,16 +226,16 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             if (it >= STAGES) PWAIT(0, &S.done[s], ((it - STAGES) / STAGES) & 1);
             if (elect_one()) {
               const int na = stage_atoms(C, kc);
-              mbar_arrive_expect_tx(&S.b_full[s], na * ((PFLAG(8) ? 0 : ATOM_BYTES) + ATOM_BYTES));
-              const int urow = (q * n_nblk + blk) * (2 * BN);
-              for (int h = 0; h < na; ++h) {
-                if (!PFLAG(8)) tma_load_3d(S.v[s][h], &map_v, &S.b_full[s], SK * kc + BK * h, m0, q);
-                tma_load_2d(S.u[s][h], &map_u, &S.b_full[s], SK * kc + BK * h, urow);
-              }
-              // V comes from HBM (the input transform just wrote it; the 3
-              // smem stages hide ~3 us less than its latency under load):
-              // prefetch the V box of stage it + V_PREFETCH into L2
-              if (V_PREFETCH > 0 && !PFLAG(8)) {
+              // the U box is always full (channels past C are TMA zero fill)
+              mbar_arrive_expect_tx(&S.b_full[s], (PFLAG(8) ? 0 : na * V_ATOM_BYTES) + U_ATOM_BYTES);
+              if (!PFLAG(8))
+                for (int h = 0; h < na; ++h) tma_load_3d(S.v[s][h], &map_v, &S.b_full[s], SK * kc + VK * h, m0, q);
+              tma_load_2d(S.u[s], &map_u, &S.b_full[s], SK * kc, (q * n_nblk + blk) * (2 * BN));
+              // V comes from HBM (the input transform just wrote it): prefetch
+              // the V box of stage it + V_PREFETCH into L2 -- once per m-block:
+              // the n_nblk CTAs of an m-block (running side by side) take turns
+              // by stage, so L2 sees no redundant prefetch requests
+              if (V_PREFETCH > 0 && !PFLAG(8) && (int)((it + V_PREFETCH) % n_nblk) == blk) {
                 int nq = q, nk = kc + V_PREFETCH, nm = m0;
                 nq += nk / KS;
                 nk %= KS;
@@ -218,7 +244,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
                   nm = (int)((w + gridDim.x) / n_nblk) * BM;
                 }
                 if (nm < d.tiles && nq < Q)
-                  for (int h = 0; h < stage_atoms(C, nk); ++h) tma_prefetch_3d(&map_v, SK * nk + BK * h, nm, nq);
+                  for (int h = 0; h < stage_atoms(C, nk); ++h) tma_prefetch_3d(&map_v, SK * nk + VK * h, nm, nq);
               }
             }
             __syncwarp();
@@ -226,54 +252,45 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
       }
     } else if (warp == WARP_MMA) {
       // ================= MMA issuer (whole warp converged, one lane issues) =================
-      // one tcgen05.commit per 64-channel stage: each commit costs the tensor
-      // pipe a ~140-cycle bubble (tools/commit_probe.cu), so the stage is the
-      // unit of every release (smem stage, A slot, accumulator chunk)
-      const uint32_t idesc128 = idesc_tf32(BM, 2 * BN), idesc64 = idesc_tf32(BM, BN);
-      uint32_t it = 0, uses0 = 0, uses1 = 0, st2 = 0;
+      // one tcgen05.commit per 64-channel stage (each commit costs the tensor
+      // pipe a ~140-cycle bubble, tools/commit_probe.cu)
+      const uint32_t idesc128 = idesc_f16(BM, 2 * BN), idesc64 = idesc_f16(BM, BN);
+      uint32_t it = 0, chunk = 0;
       for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
         for (int q = 0; q < Q; ++q) {
           for (int kc = 0; kc < KS; ++kc, ++it) {
             const uint32_t sb = it % STAGES, sa = it % A_SLOTS;
             const int na = stage_atoms(C, kc);
-            // accumulator buffers of this stage: chunk32 == 0 -> one 64-channel
-            // chunk in buffer (st2 % 2); chunk32 == 1 -> two 32-channel chunks,
-            // buffers 0 and 1
-            const uint32_t b0 = chunk32 ? 0u : (st2 & 1u);
-            const bool use0 = chunk32 || b0 == 0, use1 = chunk32 ? na == 2 : b0 == 1;
-            if (use0) { PWAIT(0, &S.acc_empty[0], (uses0 & 1) ^ 1); ++uses0; }
-            if (use1) { PWAIT(0, &S.acc_empty[1], (uses1 & 1) ^ 1); ++uses1; }
+            const bool first = kc % CHS == 0;  // a chunk starts: fresh accumulators in buffer chunk % 2
+            const uint32_t buf = chunk & 1u;
+            if (first) PWAIT(0, &S.acc_empty[buf], ((chunk >> 1) & 1) ^ 1);
             // no b_full wait: the converter signals a_full only after it
             // observed b_full, and the same TMA transaction carried U
             PWAIT(1, &S.a_full[sa], (it / A_SLOTS) & 1);
             tc_fence_after();
-            const uint32_t a_hi = tmem + COL_A + sa * (4 * BK), a_lo = a_hi + 2 * BK;
+            const uint32_t a_hi = tmem + COL_A + sa * A_COLS, a_lo = a_hi + A_COLS / 2;
+            const uint32_t dacc = tmem + COL_ACC + buf * (2 * BN);
             if (elect_one()) {
-              for (int h = 0; h < na; ++h) {
-                const uint64_t du = sdesc_sw128(smem_u32(S.u[sb][h]));
-                const uint32_t buf = chunk32 ? (uint32_t)h : b0;
-                const uint32_t dacc = tmem + COL_ACC + buf * (2 * BN);
-#pragma unroll
-                for (int k = 0; k < BK / 8; ++k) {
-                  // +32 B per K = 8 slice, in 16-byte descriptor units
-                  const bool fresh = k == 0 && (chunk32 || h == 0);
-                  mma_tf32_ts(dacc, a_hi + BK * h + 8 * k, du + 2 * k, idesc128, fresh ? 0u : 1u);
-                  if (!PFLAG(4)) mma_tf32_ts(dacc + BN, a_lo + BK * h + 8 * k, du + 2 * k, idesc64, 1u);
-                }
+              const uint64_t du = sdesc_sw128(smem_u32(S.u[sb]));
+              for (int k = 0; k < 2 * na; ++k) {
+                // +32 B per K = 16 slice, in 16-byte descriptor units
+                mma_f16_ts(dacc, a_hi + 8 * k, du + 2 * k, idesc128, (first && k == 0) ? 0u : 1u);
+                if (!PFLAG(4)) mma_f16_ts(dacc + BN, a_lo + 8 * k, du + 2 * k, idesc64, 1u);
               }
               mma_commit(&S.done[sb]);
             }
             __syncwarp();
-            ++st2;
+            if (kc % CHS == CHS - 1 || kc == KS - 1) ++chunk;
           }
         }
       }
     }
   } else if (warp < 4) {
     setmaxnreg_dec<REG_CONV>();
-    // ================= converter: V stage (smem) -> hi/lo -> TMEM A slot =================
+    // ================= converter: V stage (smem) -> s_v V -> hi/lo fp16 -> TMEM A slot =================
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * warp) << 16);
     const int m = 32 * warp + lane;
+    const f2 sv2 = pk(exp2i(sv_exp), exp2i(sv_exp));
     uint32_t it = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
       for (int q = 0; q < Q; ++q) {
@@ -281,32 +298,37 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           const uint32_t sb = it % STAGES, sa = it % A_SLOTS;
           const int na = stage_atoms(C, kc);
           PWAIT(0, &S.b_full[sb], (it / STAGES) & 1);
-          // A slot sa was last read by the MMAs of stage it - 2
+          // A slot sa was last read by the MMAs of stage it - A_SLOTS
           if (it >= A_SLOTS) PWAIT(1, &S.done[(it - A_SLOTS) % STAGES], ((it - A_SLOTS) / STAGES) & 1);
           tc_fence_after();
-          const uint32_t base = lane_addr + COL_A + sa * (4 * BK);
+          const uint32_t base = lane_addr + COL_A + sa * A_COLS;
           for (int h = 0; h < na; ++h) {
             if (PFLAG(1)) break;
-            const uint8_t* vrow = reinterpret_cast<const uint8_t*>(S.v[sb][h]);
+            const uint32_t vrow = smem_u32(S.v[sb][h]);
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              float hi[16], lo[16];
+              uint32_t hi[8], lo[8];
 #pragma unroll
               for (int c4 = 0; c4 < 4; ++c4) {
-                // row m, 16-byte chunk (4 hh + c4) of the SWIZZLE_128B tile
-                const float4 x = *reinterpret_cast<const float4*>(vrow + sw128_offset(m, 16 * hh + 4 * c4));
-                const float xs[4] = {x.x, x.y, x.z, x.w};
+                // row m, 16-byte chunk (4 hh + c4) of the SWIZZLE_128B tile: two
+                // channel pairs, scaled, split and packed with f32x2 / f16x2 ops
+                f2 x01, x23;
+                asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                             : "=l"(x01), "=l"(x23)
+                             : "r"(vrow + sw128_offset(m, 16 * hh + 4 * c4)));
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  // hi = tf32 round-to-nearest (ties away) in 2 integer ops; lo = x - hi
-                  // exactly, handed to the tensor core raw (it truncates lo to tf32)
-                  const float hv = __uint_as_float((__float_as_uint(xs[e]) + 0x1000u) & 0xFFFFE000u);
-                  hi[c4 * 4 + e] = hv;
-                  lo[c4 * 4 + e] = __fsub_rn(xs[e], hv);
+                for (int e = 0; e < 2; ++e) {
+                  const float2 p = upk(mul2(e ? x23 : x01, sv2));
+                  const __half2 h = __float22half2_rn(p);
+                  const float2 hf = __half22float2(h);
+                  const __half2 l = __float22half2_rn(upk(sub2(pk(p.x, p.y), pk(hf.x, hf.y))));
+                  hi[2 * c4 + e] = *reinterpret_cast<const uint32_t*>(&h);
+                  lo[2 * c4 + e] = *reinterpret_cast<const uint32_t*>(&l);
                 }
               }
-              tmem_st16(base + BK * h + 16 * hh, hi);
-              tmem_st16(base + 2 * BK + BK * h + 16 * hh, lo);
+              // channels 32 h + 16 hh + [0, 16) -> columns 16 h + 8 hh + [0, 8)
+              tmem_st8u(base + 16 * h + 8 * hh, hi);
+              tmem_st8u(base + A_COLS / 2 + 16 * h + 8 * hh, lo);
             }
           }
           tmem_st_wait();
@@ -318,12 +340,13 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     }
   } else {
     setmaxnreg_inc<REG_EPI>();
-    // ================= epilogue: chunks -> M_q -> Y (registers) -> y =================
+    // ================= epilogue: chunks -> M'_q -> Y (registers) -> y =================
     const int quad = warp % 4;
     const int c0 = ((warp - 4) / 4) * EC;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * quad) << 16);
     const int m = 32 * quad + lane;
-    uint32_t it = 0, st2 = 0;
+    const float inv_v = exp2i(-sv_exp);
+    uint32_t it = 0, chunk = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
       const int64_t tile = (w / n_nblk) * BM + m;
       const int n0 = (int)(w % n_nblk) * BN;
@@ -334,34 +357,32 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         for (int j = 0; j < EC; ++j) Y[p][j] = 0.f;
       for (int q = 0; q < Q; ++q) {
         float mq[EC];
-        for (int kc = 0; kc < KS; ++kc, ++it, ++st2) {
-          const int na = stage_atoms(C, kc);
+        for (int kc = 0; kc < KS; ++kc, ++it) {
+          if (!(kc % CHS == CHS - 1 || kc == KS - 1)) continue;  // chunk not complete yet
           PWAIT(0, &S.done[it % STAGES], (it / STAGES) & 1);
           tc_fence_after();
-          const int nb = chunk32 ? na : 1;
-          for (int bi = 0; bi < nb; ++bi) {
-            const uint32_t buf = chunk32 ? (uint32_t)bi : (st2 & 1u);
-            const bool first = kc == 0 && bi == 0;
-            const uint32_t acc = lane_addr + COL_ACC + buf * (2 * BN) + c0;
+          const uint32_t buf = chunk & 1u;
+          const bool first = kc < CHS;
+          const uint32_t acc = lane_addr + COL_ACC + buf * (2 * BN) + c0;
 #pragma unroll
-            for (int h = 0; h < EC / 8; ++h) {
-              if (PFLAG(2)) { mq[8 * h] = 0.f; continue; }
-              float mn[8], cr[8];
-              tmem_ld8(acc + 8 * h, mn);
-              tmem_ld8(acc + BN + 8 * h, cr);
-              tmem_ld_wait();
+          for (int h = 0; h < EC / 8; ++h) {
+            if (PFLAG(2)) { mq[8 * h] = 0.f; continue; }
+            float mn[8], cr[8];
+            tmem_ld8(acc + 8 * h, mn);
+            tmem_ld8(acc + BN + 8 * h, cr);
+            tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float part = __fadd_rn(chunk32 ? trunc_compensate(mn[j], 1u) : mn[j], cr[j]);
-                mq[8 * h + j] = first ? part : __fadd_rn(mq[8 * h + j], part);
-              }
+            for (int j = 0; j < 8; ++j) {
+              const float part = __fadd_rn(CHS == 1 ? trunc_compensate(mn[j], 1u) : mn[j], cr[j]);
+              mq[8 * h + j] = first ? part : __fadd_rn(mq[8 * h + j], part);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.acc_empty[buf]);
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.acc_empty[buf]);
+          ++chunk;
         }
-        // output transform: Y_p +-= M_q for the positions p with a nonzero coefficient
+        // output transform: Y_p +-= M'_q for the positions p with a nonzero coefficient
         const char4 cf = *reinterpret_cast<const char4*>(S.coef[q]);
         const int8_t cfa[4] = {cf.x, cf.y, cf.z, cf.w};
 #pragma unroll
@@ -375,7 +396,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           }
         }
       }
-      // Y -> y: positions (i, j) of tile (n, ty, tx), this warp's filters
+      // Y -> y: positions (i, j) of tile (n, ty, tx), this warp's filters, unscaled
       if (tile < d.tiles) {
         const int tx = (int)(tile % d.tw);
         const int64_t t2 = tile / d.tw;
@@ -388,11 +409,12 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         for (int j = 0; j < EC; ++j) {
           const int f = n0 + c0 + j;
           if (f >= F) break;
+          const float inv = __ldg(inv_f + f);
           float* yf = y + ((size_t)n * F + f) * (size_t)d.oh * d.ow + (size_t)oy * d.ow + ox;
 #pragma unroll
           for (int ii = 0; ii < 2; ++ii) {
             if (oy + ii >= d.oh) continue;
-            const float v0 = Y[2 * ii][j], v1 = Y[2 * ii + 1][j];
+            const float v0 = (Y[2 * ii][j] * inv_v) * inv, v1 = (Y[2 * ii + 1][j] * inv_v) * inv;
             float* dst = yf + ii * d.ow;
             if (vec) {
               bad |= !(isfinite(v0) && isfinite(v1));
@@ -428,6 +450,76 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
   if (warp == WARP_MMA) tmem_dealloc<512>(tmem);
 }
 
+// max|V| into the slots (the stage API's dwm_gemm_output gets V without the
+// input transform's max|x|; |V| itself is a valid bound for the scale)
+__global__ void v_absmax_kernel(const float* __restrict__ V, int64_t n, uint32_t* __restrict__ slots) {
+  uint32_t m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(V[i])));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (threadIdx.x % 32 == 0) atomicMax(slots + (blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32) % DWM_XMAX_SLOTS, m);
+}
+
+// Per-filter scale s_f = 2^(12 - floor(log2 max|w_f|)) (stored as 1 / s_f),
+// one CTA per (padded) filter; rows past F get 1.
+__global__ void filter_scale_kernel(const dwm_desc_t d, const float* __restrict__ w, FiltView fv,
+                                    float* __restrict__ inv_f) {
+  const int f = blockIdx.x;
+  uint32_t m = 0;
+  if (f < d.f) {
+    const int taps = d.r_h * d.r_w, n = d.c * taps;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int c = i / taps, t = i % taps;
+      const float v = w[(int64_t)f * fv.sf + (int64_t)c * fv.sc + (int64_t)(t / d.r_w) * fv.skh + (int64_t)(t % d.r_w) * fv.skw];
+      m = max(m, __float_as_uint(fabsf(v)));
+    }
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  __shared__ uint32_t red[32];
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)blockDim.x / 32; ++i) m = max(m, red[i]);
+    m = max(m, red[0]);
+    inv_f[f] = exp2i(-scale_exp(m));
+  }
+}
+
+// U'hi / U'lo (fp16) per 64-filter block, stacked:
+// U[((fq * nblk + f / 64) * 128 + {0: hi, 64: lo} + f % 64) * C + c]; one
+// thread per (f, c) over the padded filter count (rows past F are zeros).
+__global__ void filter_split_kernel(const dwm_desc_t d, const float* __restrict__ w, FiltView fv,
+                                    const float* __restrict__ inv_f, __half* __restrict__ U) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nblk = (d.f + BN - 1) / BN;
+  const int64_t fcp = (int64_t)nblk * BN * d.c;
+  if (idx >= fcp) return;
+  const int f = (int)(idx / d.c), c = (int)(idx % d.c);
+  const bool live = f < d.f;
+  const float s = __frcp_rn(inv_f[f]);
+  const int64_t row0 = (int64_t)(f / BN) * (2 * BN) + f % BN;
+  int fq = 0;
+  for (int rp = 0; rp < d.n_row_parts; ++rp)
+    for (int cp = 0; cp < d.n_col_parts; ++cp) {
+      float u[4][4];
+      part_filter_transform(d, w + (live ? (int64_t)f * fv.sf + (int64_t)c * fv.sc : 0), fv, rp, cp, u);
+      const int lr = d.row_parts[rp].count + 1, lc = d.col_parts[cp].count + 1;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (a < lr && b < lc) {
+            const float v = live ? u[a][b] * s : 0.f;
+            const __half hi = __float2half_rn(v);
+            const __half lo = __float2half_rn(v - __half2float(hi));
+            const int64_t o = ((int64_t)(fq + a * lc + b) * nblk * (2 * BN) + row0) * d.c + c;
+            U[o] = hi;
+            U[o + (int64_t)BN * d.c] = lo;
+          }
+      fq += lr * lc;
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -446,7 +538,7 @@ int make_v_map(CUtensorMap* map, const float* base, const dwm_desc_t& d) {
   // [freq][tiles][C]: rows past `tiles` of a frequency read as zeros
   const cuuint64_t dims[3] = {(cuuint64_t)d.c, (cuuint64_t)d.tiles, (cuuint64_t)d.num_freqs};
   const cuuint64_t strides[2] = {(cuuint64_t)d.c * sizeof(float), (cuuint64_t)d.tiles * d.c * sizeof(float)};
-  const cuuint32_t box[3] = {BK, BM, 1};
+  const cuuint32_t box[3] = {VK, BM, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -455,62 +547,90 @@ int make_v_map(CUtensorMap* map, const float* base, const dwm_desc_t& d) {
   return DWM_OK;
 }
 
-// U in the stacked tcgen05 layout: [freq][64-filter block][U_hi 64 rows; U_lo 64 rows][C]
-int make_u_map(CUtensorMap* map, const float* base, const dwm_desc_t& d) {
+// U in the stacked layout: [freq][64-filter block][U'hi 64 rows; U'lo 64 rows][C] fp16
+int make_u_map(CUtensorMap* map, const void* base, const dwm_desc_t& d) {
   auto encode = get_encode();
   if (!encode) return fail(DWM_ECUDA, "cuTensorMapEncodeTiled is unavailable");
   const int64_t nblk = (d.f + BN - 1) / BN;
   const cuuint64_t dims[2] = {(cuuint64_t)d.c, (cuuint64_t)(d.num_freqs * nblk * 2 * BN)};
-  const cuuint64_t strides[1] = {(cuuint64_t)d.c * sizeof(float)};
-  const cuuint32_t box[2] = {BK, 2 * BN};
+  const cuuint64_t strides[1] = {(cuuint64_t)d.c * 2};
+  const cuuint32_t box[2] = {SK, 2 * BN};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)base, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DWM_ECUDA, "cuTensorMapEncodeTiled(U) failed (%d)", (int)r);
   return DWM_OK;
 }
 
+size_t u_split_bytes(const dwm_desc_t& d) {
+  return (size_t)d.num_freqs * (size_t)((d.f + BN - 1) / BN) * 2 * BN * (size_t)d.c * 2;
+}
+
 }  // namespace
 
 bool tc_gemm_supported(const dwm_desc_t& d) {
-  return d.c % BK == 0 && d.f >= 1 && d.num_freqs <= MAX_FREQS && d.tiles < ((int64_t)1 << 31);
+  return d.c % VK == 0 && d.f >= 1 && d.num_freqs <= MAX_FREQS && d.tiles < ((int64_t)1 << 31);
 }
 
+// [U'hi; U'lo] fp16 planes, then one fp32 1 / s_f per padded filter
 size_t tc_filter_bytes(const dwm_desc_t& d) {
-  return (size_t)d.num_freqs * (size_t)((d.f + BN - 1) / BN) * 2 * BN * (size_t)d.c * sizeof(float);
+  return u_split_bytes(d) + (size_t)((d.f + BN - 1) / BN) * BN * sizeof(float);
 }
 
-// Accumulator chunk: one 64-channel stage when C >= 128 (emulated MSE
-// 0.35-0.61x the reference DWM32's, tools/tc_accuracy_emul.py "pair64"), two
-// 32-channel chunks per stage otherwise (C = 64: "pair64" would be one chain
-// over all of K, 1.1-1.3x).  DWM_TC_CHUNK=32|64 overrides (experiments).
-static int tc_chunk32(const dwm_desc_t& d) {
+int launch_filter_transform_f16split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s,
+                                     const int64_t* strides) {
+  const FiltView fv = strides ? FiltView{strides[0], strides[1], strides[2], strides[3]}
+                                 : FiltView{(int64_t)d.c * d.r_h * d.r_w, (int64_t)d.r_h * d.r_w, d.r_w, 1};
+  const int nblk = (d.f + BN - 1) / BN;
+  float* inv_f = reinterpret_cast<float*>(static_cast<char*>(U) + u_split_bytes(d));
+  filter_scale_kernel<<<nblk * BN, 256, 0, s>>>(d, (const float*)w, fv, inv_f);
+  const int64_t n = (int64_t)nblk * BN * d.c;
+  filter_split_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(d, (const float*)w, fv, inv_f, (__half*)U);
+  DWM_CUDA_TRY(cudaGetLastError());
+  return DWM_OK;
+}
+
+// Accumulator chunk: 128 channels (2 stages) when C >= 128, else 64 channels
+// with the +1 ulp compensation.  DWM_TC_CHUNK=64|128 overrides (experiments).
+static int tc_chunk_stages(const dwm_desc_t& d) {
   static const int env = [] {
     const char* e = getenv("DWM_TC_CHUNK");
     return e ? atoi(e) : 0;
   }();
-  if (env == 32) return 1;
-  if (env == 64) return 0;
-  return d.c >= 128 ? 0 : 1;
+  if (env == 64) return 1;
+  if (env == 128) return 2;
+  return d.c >= 128 ? 2 : 1;
 }
 
-int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag, cudaStream_t s) {
+int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag, const uint32_t* xmax,
+                   void* scratch, size_t scratch_bytes, cudaStream_t s) {
   if (!tc_gemm_supported(d)) return fail(DWM_EUNSUPPORTED, "tcgen05 GEMM needs C %% 32 == 0");
+  if (!xmax) {
+    // no input-transform range: bound the scale by max|V| itself
+    if (!scratch || scratch_bytes < DWM_XMAX_BYTES)
+      return fail(DWM_EINVAL_SHAPE, "tcgen05 GEMM on a caller V needs %d bytes of workspace (got %zu)",
+                  (int)DWM_XMAX_BYTES, scratch_bytes);
+    DWM_CUDA_TRY(cudaMemsetAsync(scratch, 0, DWM_XMAX_BYTES, s));
+    const int64_t n = (int64_t)d.num_freqs * d.tiles * d.c;
+    v_absmax_kernel<<<1184, 256, 0, s>>>((const float*)V, n, (uint32_t*)scratch);
+    xmax = (const uint32_t*)scratch;
+  }
   CUtensorMap mv, mu;
   if (int st = make_v_map(&mv, (const float*)V, d)) return st;
-  if (int st = make_u_map(&mu, (const float*)U, d)) return st;
+  if (int st = make_u_map(&mu, U, d)) return st;
+  const float* inv_f = reinterpret_cast<const float*>(static_cast<const char*>(U) + u_split_bytes(d));
   const size_t smem = sizeof(Smem) + 1024;
   int sms = 0;
   if (int st = device_sm_count(&sms)) return st;
   const int64_t items = ((d.tiles + BM - 1) / BM) * ((d.f + BN - 1) / BN);
   const int grid = (int)(items < sms ? items : sms);
-  if (tc_chunk32(d)) {
-    if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<true>, smem)) return st;
-    gemm_tc_kernel<true><<<grid, THREADS, smem, s>>>(d, mv, mu, (float*)y, flag);
+  if (tc_chunk_stages(d) == 2) {
+    if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<2>, smem)) return st;
+    gemm_tc_kernel<2><<<grid, THREADS, smem, s>>>(d, mv, mu, inv_f, xmax, (float*)y, flag);
   } else {
-    if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<false>, smem)) return st;
-    gemm_tc_kernel<false><<<grid, THREADS, smem, s>>>(d, mv, mu, (float*)y, flag);
+    if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<1>, smem)) return st;
+    gemm_tc_kernel<1><<<grid, THREADS, smem, s>>>(d, mv, mu, inv_f, xmax, (float*)y, flag);
   }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;

@@ -9,12 +9,19 @@ namespace dwm {
 // strides: element strides (f, c, kh, kw) of the weight view; NULL = contiguous F,C,r_h,r_w
 int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void* U, cudaStream_t s,
                             const int64_t* strides = nullptr);
-// U for the tcgen05 path: TF32-valued RN split U_hi / U_lo, stacked per
-// 64-filter block: [freq][ceil(F/64)][U_hi 64 rows; U_lo 64 rows][C] (zero rows
-// past F), so one TMA box gives the GEMM its [U_hi; U_lo] N = 128 B operand.
-int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s,
-                                      const int64_t* strides = nullptr);
-int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s);
+// U for the tcgen05 path: per-filter power-of-two scaled, fp16 split U'hi /
+// U'lo, stacked per 64-filter block: [freq][ceil(F/64)][U'hi 64 rows; U'lo 64
+// rows][C] fp16 (zero rows past F), so one TMA box gives the GEMM its
+// [U'hi; U'lo] N = 128 B operand; then 1 / s_f per padded filter (fp32).
+int launch_filter_transform_f16split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s,
+                                     const int64_t* strides = nullptr);
+// max|x| slots the float input transform fills when xmax != NULL (zeroed
+// first, on the same stream): the tcgen05 GEMM's V-scale bound
+constexpr int DWM_XMAX_SLOTS = 128;
+constexpr size_t DWM_XMAX_BYTES = DWM_XMAX_SLOTS * sizeof(uint32_t);
+static_assert(DWM_XMAX_BYTES == DWM_RANGE_BYTES, "C ABI range size");
+int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s,
+                           uint32_t* xmax = nullptr);
 int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void* U, void* y,
                       int32_t* flag, cudaStream_t s);
 int weight_grad_splits(const dwm_desc_t& d);
@@ -29,7 +36,9 @@ int launch_small_c(const dwm_desc_t& d, const void* x, const void* U, void* y, i
                    cudaStream_t s);
 bool tc_gemm_supported(const dwm_desc_t& d);
 size_t tc_filter_bytes(const dwm_desc_t& d);
-int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag,
-                   cudaStream_t s);
+// xmax: the input transform's max|x| slots for V; NULL = bound by max|V|,
+// computed into scratch (>= DWM_XMAX_BYTES)
+int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag, const uint32_t* xmax,
+                   void* scratch, size_t scratch_bytes, cudaStream_t s);
 
 }  // namespace dwm

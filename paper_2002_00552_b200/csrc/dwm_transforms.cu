@@ -10,6 +10,7 @@
 // reference's binary32/binary64 values (the coefficients are 0, +-1, +-1/2).
 #include "dwm_common.cuh"
 #include "dwm_kernels.h"
+#include "dwm_filter.cuh"
 #include "dwm_wino.cuh"
 
 #include <algorithm>
@@ -21,55 +22,6 @@ namespace dwm {
 // ---------------------------------------------------------------------------
 // Filter transform: one thread per (f, c); U[fq][f][c].
 // ---------------------------------------------------------------------------
-// Element strides of the weight view the filter transforms read: (f, c, kh, kw).
-// The forward passes the contiguous F,C,r_h,r_w layout; the backward's data
-// gradient passes the channel-transposed, tap-reversed polyphase sub-kernels
-// w[:, :, rho::s_h, sig::s_w] (negative tap strides) without materialising them.
-struct FiltView {
-  int64_t sf, sc, skh, skw;
-};
-__host__ __device__ inline FiltView contiguous_view(const dwm_desc_t& d) {
-  return FiltView{(int64_t)d.c * d.r_h * d.r_w, (int64_t)d.r_h * d.r_w, d.r_w, 1};
-}
-
-template <typename T>
-__device__ __forceinline__ void part_filter_transform(const dwm_desc_t& d, const T* __restrict__ wfc, const FiltView& fv,
-                                                      int rp, int cp, T out[4][4]) {
-  const dwm_axis_part_t R = d.row_parts[rp], Cc = d.col_parts[cp];
-  const int pr = R.count, pc = Cc.count;
-  T g[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      g[i][j] = (i < pr && j < pc)
-                    ? wfc[(int64_t)(R.origin + R.step * i) * fv.skh + (int64_t)(Cc.origin + Cc.step * j) * fv.skw]
-                    : T(0);
-  // row stage: t[u][j] = sum_i G_r[u][i] * g[i][j]
-  T t[4][3];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      T acc = mul_rn((T)c_g[pr][u][0], g[0][j]);
-#pragma unroll
-      for (int i = 1; i < 3; ++i)
-        if (i < pr) acc = fma_rn((T)c_g[pr][u][i], g[i][j], acc);
-      t[u][j] = acc;
-    }
-  // column stage: U[u][v] = sum_j t[u][j] * G_c[v][j]
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      T acc = mul_rn(t[u][0], (T)c_g[pc][v][0]);
-#pragma unroll
-      for (int j = 1; j < 3; ++j)
-        if (j < pc) acc = fma_rn(t[u][j], (T)c_g[pc][v][j], acc);
-      out[u][v] = acc;
-    }
-}
-
 template <typename T>
 __global__ void filter_transform_kernel(const dwm_desc_t d, const T* __restrict__ w, const FiltView fv,
                                         T* __restrict__ U) {
@@ -92,47 +44,6 @@ __global__ void filter_transform_kernel(const dwm_desc_t d, const T* __restrict_
     }
 }
 
-__device__ __forceinline__ float tf32_rn(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-// U_hi = tf32(U), U_lo = tf32(U - U_hi), stacked per 64-filter block:
-// U[((fq * nblk + f / 64) * 128 + {0: hi, 64: lo} + f % 64) * C + c]; one
-// thread per (f, c) over the padded filter count (rows past F are zeros).
-__global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const float* __restrict__ w, const FiltView fv,
-                                                  float* __restrict__ U) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int nblk = (d.f + 63) / 64;
-  const int64_t fcp = (int64_t)nblk * 64 * d.c;
-  if (idx >= fcp) return;
-  const int f = (int)(idx / d.c), c = (int)(idx % d.c);
-  const bool live = f < d.f;
-  const float* wfc = w + (live ? (int64_t)f * fv.sf + (int64_t)c * fv.sc : 0);
-  const int64_t row0 = (int64_t)(f / 64) * 128 + f % 64;
-  int fq = 0;
-  for (int rp = 0; rp < d.n_row_parts; ++rp)
-    for (int cp = 0; cp < d.n_col_parts; ++cp) {
-      float u[4][4];
-      part_filter_transform(d, wfc, fv, rp, cp, u);
-      const int lr = d.row_parts[rp].count + 1, lc = d.col_parts[cp].count + 1;
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (a < lr && b < lc) {
-            const float v = live ? u[a][b] : 0.f;
-            const float hi = tf32_rn(v);
-            const float lo = tf32_rn(v - hi);
-            const int64_t o = ((int64_t)(fq + a * lc + b) * nblk * 128 + row0) * d.c + c;
-            U[o] = hi;
-            U[o + 64 * (int64_t)d.c] = lo;
-          }
-      fq += lr * lc;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Input transform: one thread per (tile, c), c fastest; V[fq][tile][c].
 // Window sample (i, j) of part (rp, cp) for tile (ty, tx) is padded-input
@@ -140,8 +51,17 @@ __global__ void filter_transform_tf32split_kernel(const dwm_desc_t d, const floa
 // when it falls in the padding or past the part's strided slice
 // (k >= OUT-1+count: the reference's even-extension zeros, engines.py:109-115).
 // ---------------------------------------------------------------------------
+// max|x| of the staged input (the tcgen05 GEMM's operand-scale bound):
+// one atomicMax per warp into DWM_XMAX_SLOTS spread slots (float bits of a
+// non-negative value order like unsigned integers).
+__device__ __forceinline__ void xmax_reduce(float amax, unsigned mask, uint32_t* xmax, unsigned spread) {
+  const uint32_t m = __reduce_max_sync(mask, __float_as_uint(amax));
+  if ((threadIdx.x % 32) == (unsigned)(__ffs(mask) - 1)) atomicMax(xmax + spread % DWM_XMAX_SLOTS, m);
+}
+
 template <typename T>
-__global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V) {
+__global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V,
+                                       uint32_t* __restrict__ xmax) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= d.tiles * d.c) return;
   const int c = (int)(idx % d.c);
@@ -152,6 +72,7 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
   const int n = (int)(t2 / d.th);
   const T* xc = x + ((int64_t)n * d.c + c) * d.h * d.w;
   const int64_t tc_stride = d.tiles * d.c;
+  float amax = 0.f;
   int fq = 0;
   for (int rp = 0; rp < d.n_row_parts; ++rp) {
     const dwm_axis_part_t R = d.row_parts[rp];
@@ -179,6 +100,12 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           win[i][j] = (rows[i] >= 0 && cols[j] >= 0) ? __ldg(xc + (int64_t)rows[i] * d.w + cols[j]) : T(0);
+      if (xmax) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) amax = fmaxf(amax, fabsf((float)win[i][j]));
+      }
       // row stage t[a][j] = sum_i Bt_r[a][i] win[i][j]; column stage v[a][b] = sum_j t[a][j] Bt_c[b][j]
       T t[4][4];
 #pragma unroll
@@ -205,6 +132,7 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
       fq += lr * lc;
     }
   }
+  if (xmax) xmax_reduce(amax, __activemask(), xmax, (unsigned)(idx / 32));
 }
 
 // ---------------------------------------------------------------------------
@@ -268,7 +196,7 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
 template <typename T, bool WIDE, bool STREAM, int CB>
 __global__ void __maxnreg__(DWM_IT_MAXNREG)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
-                            int twb_arg, int ws_arg, int trows_arg, int n0) {
+                            int twb_arg, int ws_arg, int trows_arg, int n0, uint32_t* __restrict__ xmax) {
   // WIDE == false: whole rows staged (ws == W, trows tile rows per CTA) -- the
   // common case, compiled without any of the column-block arithmetic
   const int twb = WIDE ? twb_arg : d.tw;
@@ -292,6 +220,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 
   // stage rows row0 .. row0 + rows_staged - 1 (zero outside [0, H))
   constexpr int VEC = 16 / sizeof(T);
+  float amax = 0.f;  // max|x| staged (float path; NaN-blind -- NaN reaches V and the flag anyway)
   if (!WIDE && d.w % VEC == 0 && ((uintptr_t)x & 15) == 0) {
     // 16-byte loads over the flattened (channel, row, vector) space, four per
     // thread in flight before the first smem store waits on one
@@ -327,6 +256,10 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
         memcpy(v, &q[u], 16);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) sx[dsto[u] + e] = v[e];
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) amax = fmaxf(amax, fabsf((float)v[e]));
+        }
       }
     }
   } else {
@@ -339,12 +272,15 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
         const T* src = xc + (int64_t)(rok ? row : 0) * d.w;
         for (int sc = threadIdx.x % 32; sc < ws; sc += 32) {
           const int col = cbase + sc;
-          dst[r * ws + sc] = (rok && col >= 0 && col < d.w) ? __ldg(src + col) : T(0);
+          const T v = (rok && col >= 0 && col < d.w) ? __ldg(src + col) : T(0);
+          dst[r * ws + sc] = v;
+          if constexpr (sizeof(T) == 4) amax = fmaxf(amax, fabsf((float)v));
         }
       }
     }
   }
   __syncthreads();
+  if (xmax) xmax_reduce(amax, 0xffffffffu, xmax, blockIdx.x * 7 + blockIdx.y * 13 + threadIdx.x / 32);
 
   constexpr int TPW = 32 / CB;  // tiles per warp step
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nwarps = blockDim.x / 32;
@@ -435,17 +371,9 @@ int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void*
   return DWM_OK;
 }
 
-int launch_filter_transform_tf32split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s,
-                                      const int64_t* strides) {
-  const int64_t n = (int64_t)((d.f + 63) / 64) * 64 * d.c;
-  const FiltView fv = strides ? FiltView{strides[0], strides[1], strides[2], strides[3]} : contiguous_view(d);
-  filter_transform_tf32split_kernel<<<grid_for(n, 128), 128, 0, s>>>(d, (const float*)w, fv, (float*)U);
-  DWM_CUDA_TRY(cudaGetLastError());
-  return DWM_OK;
-}
-
 template <typename T, int CB>
-static int launch_input_smem_cb(const dwm_desc_t& d, const void* x, void* V, cudaStream_t s, bool* used) {
+static int launch_input_smem_cb(const dwm_desc_t& d, const void* x, void* V, cudaStream_t s, bool* used,
+                                uint32_t* xmax) {
   // rows a tile row reads: (largest tap origin + s*count) over row parts = r_h + s_h - 1, +1
   int rows = 0;
   for (int i = 0; i < d.n_row_parts; ++i)
@@ -503,30 +431,33 @@ static int launch_input_smem_cb(const dwm_desc_t& d, const void* x, void* V, cud
   for (int n0 = 0; n0 < d.n; n0 += imgs_per_launch) {
     const int nb = min(imgs_per_launch, d.n - n0);
     const dim3 grid((unsigned)((d.c + CB - 1) / CB), (unsigned)(nb * per_img));
-    kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows, n0);
+    kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows, n0, xmax);
     DWM_CUDA_TRY(cudaGetLastError());
   }
   *used = true;
   return DWM_OK;
 }
 
-int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s) {
+int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s,
+                           uint32_t* xmax) {
   bool used = false;
+  if (dtype == DWM_F64) xmax = nullptr;
+  if (xmax) DWM_CUDA_TRY(cudaMemsetAsync(xmax, 0, DWM_XMAX_BYTES, s));
   // 16-channel CTAs: DWM_IT_CB=16 (experiments) or the rule below
   static const int env_cb = [] {
     const char* e = getenv("DWM_IT_CB");
     return e ? atoi(e) : 0;
   }();
   const bool cb16 = env_cb ? env_cb == 16 : it_prefers_cb16(d);
-  const int st = dtype == DWM_F64 ? launch_input_smem_cb<double, 32>(d, x, V, s, &used)
-               : cb16             ? launch_input_smem_cb<float, 16>(d, x, V, s, &used)
-                                  : launch_input_smem_cb<float, 32>(d, x, V, s, &used);
+  const int st = dtype == DWM_F64 ? launch_input_smem_cb<double, 32>(d, x, V, s, &used, nullptr)
+               : cb16             ? launch_input_smem_cb<float, 16>(d, x, V, s, &used, xmax)
+                                  : launch_input_smem_cb<float, 32>(d, x, V, s, &used, xmax);
   if (st || used) return st;
   const int64_t n = d.tiles * d.c;
   if (dtype == DWM_F64)
-    input_transform_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(d, (const double*)x, (double*)V);
+    input_transform_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(d, (const double*)x, (double*)V, nullptr);
   else
-    input_transform_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(d, (const float*)x, (float*)V);
+    input_transform_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(d, (const float*)x, (float*)V, xmax);
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }

@@ -21,6 +21,10 @@ keys = ["gpu__time_duration.sum", "launch__registers_per_thread", "sm__warps_act
 units = dict(zip(hdr, rows[1]))
 for k in keys:
     if k in d: print(f"{k:80s} {d[k]} {units.get(k, '')}")
+for k in sorted(d):  # L2 / fabric throughput breakdown
+    if (k.startswith("lts__throughput") or k.startswith("lts__t_bytes") or k.startswith("lts__d_") or
+            k.startswith("lts__t_sectors_op") or k.startswith("l1tex__m_xbar2l1tex")) and k not in keys:
+        print(f"{k:80s} {d[k]} {units.get(k, '')}")
 st = [(h.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(v.replace(",", "") or 0)) for h, v in d.items()
       if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")]
 tot = sum(v for _, v in st) or 1

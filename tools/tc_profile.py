@@ -28,6 +28,7 @@ flag = torch.zeros(1, dtype=torch.int32, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 V = ws.data_ptr()
 U = V + (desc.num_freqs * desc.tiles * desc.c * 4 + 255) // 256 * 256
+R = U + (lib.dwm_filter_bytes(desc, 0, 2) + 255) // 256 * 256  # max|x| range slots (after V and U)
 _native.check(lib.dwm_conv2d_forward(desc, 0, 2, x.data_ptr(), w.data_ptr(), y.data_ptr(), V, ws_bytes,
                                      flag.data_ptr(), s))
 buf = (ctypes.c_ulonglong * 32)()
@@ -39,7 +40,7 @@ for flags in [0, 1, 2, 4, 8, 1 | 2, 1 | 2 | 8, 1 | 2 | 4 | 8]:
     lib.dwm_debug_tc_profile(buf, 1)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()
-    _native.check(lib.dwm_gemm_output(desc, 0, 2, V, U, y.data_ptr(), flag.data_ptr(), None, 0, s))
+    _native.check(lib.dwm_gemm_output_tc(desc, V, U, R, y.data_ptr(), flag.data_ptr(), s))
     ev[1].record()
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1])
