@@ -48,10 +48,13 @@
 //   WG1/2 warps 4-11 epilogue (192 regs): tcgen05.ld chunk accumulators ->
 //                   M'_q -> Y (registers) -> y (NCHW), non-finite flag.  TMEM
 //                   lane quadrant = warp % 4, filter half = (warp - 4) / 4.
-//   WG3 warp 12     TMA producer (56 regs): V [128 tiles][2 x 32 ch] fp32 and
-//                   [U'hi; U'lo] [128 rows][64 ch] fp16 per (frequency, 64-channel) stage
+//   WG3 warp 12     V TMA producer (56 regs): V [128 tiles][2 x 32 ch] fp32 per
+//                   (frequency, 64-channel) stage into the V ring, which the
+//                   converter frees as soon as it has read a stage
 //       warp 13     TMEM allocator + MMA issuer (elect.sync from the converged warp)
-//       warps 14-15 idle (warpgroup padding for setmaxnreg)
+//       warp 14     U TMA producer: [U'hi; U'lo] [128 rows][64 ch] fp16 per
+//                   stage into the U ring, freed by the stage's MMA commit
+//       warp 15     idle (warpgroup padding for setmaxnreg)
 // TMEM columns: accumulators 2 x 128 (0-255: main | corr), A slots 4 x 64
 // (256-511: V'hi 32 | V'lo 32, two fp16 channels per column).
 #include <cuda.h>
@@ -75,33 +78,52 @@ constexpr int BM = 128;        // tiles per work item (MMA M, TMEM lanes)
 constexpr int BN = 64;         // filters per work item
 constexpr int VK = 32;         // fp32 V channels per SW128 atom (128 B rows)
 constexpr int SK = 64;         // channels per pipeline stage (2 V atoms, 1 U atom)
-constexpr int STAGES = 4;      // smem ring: 4 x (V 32 KB + U 16 KB)
+#ifndef DWM_TC_VSTAGES
+#define DWM_TC_VSTAGES 4
+#endif
+constexpr int VSTAGES = DWM_TC_VSTAGES;  // V ring: 32 KB stages, freed by the converter
+constexpr int STAGES = 4;      // U ring (16 KB stages) = commit ring, freed by the MMAs
 constexpr int A_SLOTS = 4;     // TMEM A ring: 4 x (hi 32 | lo 32) columns
 #ifndef DWM_TC_VPF
 #define DWM_TC_VPF 4
 #endif
 constexpr int V_PREFETCH = DWM_TC_VPF;  // stages of V prefetched into L2 ahead of the TMA loads
-constexpr int THREADS = 512;
+#ifndef DWM_TC_CONV_WARPS
+#define DWM_TC_CONV_WARPS 4
+#endif
+// 4: one 64-channel row per thread; 8: one 32-channel atom (measured no faster:
+// the converter stays ~75 % busy with twice the warps, and the epilogue then
+// gets 184 registers and spills -- profiles/r2/ab_tc_conv8.txt)
+constexpr int CONV_WARPS = DWM_TC_CONV_WARPS;
 constexpr int EPI_WARPS = 8;
+constexpr int EPI_WARP0 = CONV_WARPS;
+constexpr int THREADS = 32 * (CONV_WARPS + EPI_WARPS + 4);
 constexpr int EC = 32;         // filter columns per epilogue warp
-constexpr int WARP_TMA = 12, WARP_MMA = 13;
+constexpr int WARP_TMA = CONV_WARPS + EPI_WARPS, WARP_MMA = WARP_TMA + 1, WARP_UTMA = WARP_TMA + 2;
 constexpr int MAX_FREQS = 1024;
 constexpr uint32_t V_ATOM_BYTES = BM * VK * 4;   // 16 KB: [128 rows][32 fp32 ch]
 constexpr uint32_t U_ATOM_BYTES = 2 * BN * SK * 2;  // 16 KB: [128 rows][64 fp16 ch]
 constexpr uint32_t COL_ACC = 0, COL_A = 256, A_COLS = 64;
-constexpr int REG_CONV = 72, REG_EPI = 192, REG_CTRL = 56;
-static_assert(4 * 32 * (REG_CONV + REG_CTRL) + 8 * 32 * REG_EPI <= 65536, "register file");
+// setmaxnreg moves registers within the CTA's launch allocation (THREADS x the
+// compiled count: 128 at 512 threads, 96 at 640), so the budgets must fit it
+constexpr int REG_CONV = CONV_WARPS == 8 ? 40 : 72, REG_EPI = CONV_WARPS == 8 ? 184 : 192,
+              REG_CTRL = CONV_WARPS == 8 ? 32 : 56;
+constexpr int REG_LAUNCH = CONV_WARPS == 8 ? 96 : 128;
+static_assert(32 * (CONV_WARPS * REG_CONV + 4 * REG_CTRL + EPI_WARPS * REG_EPI) <= THREADS * REG_LAUNCH,
+              "register budgets exceed the launch allocation");
 
 struct __align__(1024) Smem {
-  float v[STAGES][2][BM * VK];      // [stage][atom][128 tiles][32 ch] fp32
+  float v[VSTAGES][2][BM * VK];     // [stage][atom][128 tiles][32 ch] fp32
   uint16_t u[STAGES][2 * BN * SK];  // [stage][U'hi 64 rows; U'lo 64 rows][64 ch] fp16
-  uint64_t b_full[STAGES];          // TMA -> converter (V) and MMA (U)
-  uint64_t done[STAGES];            // MMA commit per stage -> TMA, converter, epilogue
+  uint64_t v_full[VSTAGES];         // V TMA -> converter
+  uint64_t v_empty[VSTAGES];        // converter (V read) -> V TMA
+  uint64_t u_full[STAGES];          // U TMA -> MMA
+  uint64_t done[STAGES];            // MMA commit per stage -> U TMA, converter, epilogue
   uint64_t a_full[A_SLOTS];         // converter -> MMA
   uint64_t acc_empty[2];            // epilogue -> MMA
   uint32_t tmem_base;
   uint32_t xmax[2];                 // max|x| bits, reduced from the input transform's slots
-  int8_t coef[MAX_FREQS][4];
+  uint8_t coef[MAX_FREQS];           // output-transform sign of the 4 tile positions, 2 bits each
 };
 
 __device__ __forceinline__ int at_coef_rt(int r, int i, int a) {
@@ -139,6 +161,18 @@ __device__ __forceinline__ float trunc_compensate(float x, uint32_t k) {
   return __uint_as_float(__float_as_uint(x) + k);
 }
 
+// x - hi for a pair (hi = the f16x2 rounding of x), exact in fp32: two
+// mixed-precision FMAs (FHFMA, f16 operand from a register half) instead of
+// unpacking hi to fp32 first.
+__device__ __forceinline__ float2 residual_f16x2(uint32_t hi, float2 x) {
+  float2 r;
+  asm("{\n\t.reg .f16 a, b, m1;\n\tmov.b32 {a, b}, %2;\n\tmov.b16 m1, 0xBC00;\n\t"
+      "fma.rn.f32.f16 %0, a, m1, %3;\n\tfma.rn.f32.f16 %1, b, m1, %4;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(hi), "f"(x.x), "f"(x.y));
+  return r;
+}
+
 // Power-of-two operand scale from the bits of a max |value| (floor(log2) = e):
 // s = 2^(12 - e), clamped to normal floats; 0 -> 1; inf/nan -> tiny (the
 // non-finite values propagate to y and the flag).
@@ -171,11 +205,15 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
 
   // ---- one-time setup
   if (tid == 0) {
+    for (int i = 0; i < VSTAGES; ++i) {
+      mbar_init(&S.v_full[i], 1);
+      mbar_init(&S.v_empty[i], CONV_WARPS);
+    }
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&S.b_full[i], 1);
+      mbar_init(&S.u_full[i], 1);
       mbar_init(&S.done[i], 1);
     }
-    for (int i = 0; i < A_SLOTS; ++i) mbar_init(&S.a_full[i], 4);
+    for (int i = 0; i < A_SLOTS; ++i) mbar_init(&S.a_full[i], CONV_WARPS);
     for (int i = 0; i < 2; ++i) mbar_init(&S.acc_empty[i], EPI_WARPS);
     fence_barrier_init();
   }
@@ -194,8 +232,10 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         if (rem < nq) { pr = cr; pc = cc; a = rem / (cc + 1); b = rem % (cc + 1); found = 1; break; }
         rem -= nq;
       }
+    uint32_t code = 0;  // 2 bits per position p = 2 i + j: 0 -> 0, 1 -> +1, 3 -> -1
     for (int i = 0; i < 2; ++i)
-      for (int j = 0; j < 2; ++j) S.coef[q][i * 2 + j] = (int8_t)(at_coef_rt(pr, i, a) * at_coef_rt(pc, j, b));
+      for (int j = 0; j < 2; ++j) code |= ((uint32_t)(at_coef_rt(pr, i, a) * at_coef_rt(pc, j, b)) & 3u) << (2 * (2 * i + j));
+    S.coef[q] = (uint8_t)code;
   }
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch_desc(&map_v);
@@ -212,25 +252,26 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
   const long long t_start = clock64();
 #endif
 
-  if (warp >= 12) {
+  if (warp >= WARP_TMA) {
     setmaxnreg_dec<REG_CTRL>();
     if (warp == WARP_TMA) {
-      // ================= TMA producer (whole warp converged, one lane issues) =================
+      // ================= V TMA producer (whole warp converged, one lane issues) =================
+      // runs up to VSTAGES stages ahead of the converter, independent of the MMAs
       uint32_t it = 0;
       for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
         const int blk = (int)(w % n_nblk);
         const int m0 = (int)(w / n_nblk) * BM;
         for (int q = 0; q < Q; ++q)
           for (int kc = 0; kc < KS; ++kc, ++it) {
-            const uint32_t s = it % STAGES;
-            if (it >= STAGES) PWAIT(0, &S.done[s], ((it - STAGES) / STAGES) & 1);
+            const uint32_t s = it % VSTAGES;
+            if (it >= VSTAGES) PWAIT(0, &S.v_empty[s], ((it - VSTAGES) / VSTAGES) & 1);
             if (elect_one()) {
               const int na = stage_atoms(C, kc);
-              // the U box is always full (channels past C are TMA zero fill)
-              mbar_arrive_expect_tx(&S.b_full[s], (PFLAG(8) ? 0 : na * V_ATOM_BYTES) + U_ATOM_BYTES);
-              if (!PFLAG(8))
-                for (int h = 0; h < na; ++h) tma_load_3d(S.v[s][h], &map_v, &S.b_full[s], SK * kc + VK * h, m0, q);
-              tma_load_2d(S.u[s], &map_u, &S.b_full[s], SK * kc, (q * n_nblk + blk) * (2 * BN));
+              if (PFLAG(8)) mbar_arrive(&S.v_full[s]);
+              else {
+                mbar_arrive_expect_tx(&S.v_full[s], na * V_ATOM_BYTES);
+                for (int h = 0; h < na; ++h) tma_load_3d(S.v[s][h], &map_v, &S.v_full[s], SK * kc + VK * h, m0, q);
+              }
               // V comes from HBM (the input transform just wrote it): prefetch
               // the V box of stage it + V_PREFETCH into L2 -- once per m-block:
               // the n_nblk CTAs of an m-block (running side by side) take turns
@@ -250,6 +291,23 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             __syncwarp();
           }
       }
+    } else if (warp == WARP_UTMA) {
+      // ================= U TMA producer: [U'hi; U'lo] of (frequency, 64 channels, n-block) =================
+      uint32_t it = 0;
+      for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+        const int blk = (int)(w % n_nblk);
+        for (int q = 0; q < Q; ++q)
+          for (int kc = 0; kc < KS; ++kc, ++it) {
+            const uint32_t s = it % STAGES;
+            if (it >= STAGES) mbar_wait(&S.done[s], ((it - STAGES) / STAGES) & 1);
+            if (elect_one()) {
+              // the U box is always full (channels past C are TMA zero fill)
+              mbar_arrive_expect_tx(&S.u_full[s], U_ATOM_BYTES);
+              tma_load_2d(S.u[s], &map_u, &S.u_full[s], SK * kc, (q * n_nblk + blk) * (2 * BN));
+            }
+            __syncwarp();
+          }
+      }
     } else if (warp == WARP_MMA) {
       // ================= MMA issuer (whole warp converged, one lane issues) =================
       // one tcgen05.commit per 64-channel stage (each commit costs the tensor
@@ -264,9 +322,8 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             const bool first = kc % CHS == 0;  // a chunk starts: fresh accumulators in buffer chunk % 2
             const uint32_t buf = chunk & 1u;
             if (first) PWAIT(0, &S.acc_empty[buf], ((chunk >> 1) & 1) ^ 1);
-            // no b_full wait: the converter signals a_full only after it
-            // observed b_full, and the same TMA transaction carried U
             PWAIT(1, &S.a_full[sa], (it / A_SLOTS) & 1);
+            PWAIT(2, &S.u_full[sb], (it / STAGES) & 1);
             tc_fence_after();
             const uint32_t a_hi = tmem + COL_A + sa * A_COLS, a_lo = a_hi + A_COLS / 2;
             const uint32_t dacc = tmem + COL_ACC + buf * (2 * BN);
@@ -285,24 +342,26 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         }
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < CONV_WARPS) {
     setmaxnreg_dec<REG_CONV>();
     // ================= converter: V stage (smem) -> s_v V -> hi/lo fp16 -> TMEM A slot =================
-    const uint32_t lane_addr = tmem + ((uint32_t)(32 * warp) << 16);
-    const int m = 32 * warp + lane;
+    // TMEM lane quadrant warp % 4 (rows m); with 8 warps, V atom warp / 4 (32 channels) each
+    const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp % 4)) << 16);
+    const int m = 32 * (warp % 4) + lane;
+    const int h0 = CONV_WARPS == 8 ? warp / 4 : 0, hstep = CONV_WARPS == 8 ? 2 : 1;
     const f2 sv2 = pk(exp2i(sv_exp), exp2i(sv_exp));
     uint32_t it = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
       for (int q = 0; q < Q; ++q) {
         for (int kc = 0; kc < KS; ++kc, ++it) {
-          const uint32_t sb = it % STAGES, sa = it % A_SLOTS;
+          const uint32_t sb = it % VSTAGES, sa = it % A_SLOTS;
           const int na = stage_atoms(C, kc);
-          PWAIT(0, &S.b_full[sb], (it / STAGES) & 1);
+          PWAIT(0, &S.v_full[sb], (it / VSTAGES) & 1);
           // A slot sa was last read by the MMAs of stage it - A_SLOTS
           if (it >= A_SLOTS) PWAIT(1, &S.done[(it - A_SLOTS) % STAGES], ((it - A_SLOTS) / STAGES) & 1);
           tc_fence_after();
           const uint32_t base = lane_addr + COL_A + sa * A_COLS;
-          for (int h = 0; h < na; ++h) {
+          for (int h = h0; h < na; h += hstep) {
             if (PFLAG(1)) break;
             const uint32_t vrow = smem_u32(S.v[sb][h]);
 #pragma unroll
@@ -320,9 +379,9 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
                 for (int e = 0; e < 2; ++e) {
                   const float2 p = upk(mul2(e ? x23 : x01, sv2));
                   const __half2 h = __float22half2_rn(p);
-                  const float2 hf = __half22float2(h);
-                  const __half2 l = __float22half2_rn(upk(sub2(pk(p.x, p.y), pk(hf.x, hf.y))));
-                  hi[2 * c4 + e] = *reinterpret_cast<const uint32_t*>(&h);
+                  const uint32_t hu = *reinterpret_cast<const uint32_t*>(&h);
+                  const __half2 l = __float22half2_rn(residual_f16x2(hu, p));
+                  hi[2 * c4 + e] = hu;
                   lo[2 * c4 + e] = *reinterpret_cast<const uint32_t*>(&l);
                 }
               }
@@ -331,6 +390,9 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
               tmem_st8u(base + A_COLS / 2 + 16 * h + 8 * hh, lo);
             }
           }
+          // every V value of the stage is in registers (consumed above): free the V slot
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.v_empty[sb]);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
@@ -342,7 +404,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     setmaxnreg_inc<REG_EPI>();
     // ================= epilogue: chunks -> M'_q -> Y (registers) -> y =================
     const int quad = warp % 4;
-    const int c0 = ((warp - 4) / 4) * EC;
+    const int c0 = ((warp - EPI_WARP0) / 4) * EC;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * quad) << 16);
     const int m = 32 * quad + lane;
     const float inv_v = exp2i(-sv_exp);
@@ -356,6 +418,9 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
 #pragma unroll
         for (int j = 0; j < EC; ++j) Y[p][j] = 0.f;
       for (int q = 0; q < Q; ++q) {
+        // output transform below: Y_p +-= M'_q for the positions p with a
+        // nonzero coefficient (2-bit codes: 1 -> +1, 3 -> -1)
+        const uint32_t cf = S.coef[q];
         float mq[EC];
         for (int kc = 0; kc < KS; ++kc, ++it) {
           if (!(kc % CHS == CHS - 1 || kc == KS - 1)) continue;  // chunk not complete yet
@@ -366,7 +431,7 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           const uint32_t acc = lane_addr + COL_ACC + buf * (2 * BN) + c0;
 #pragma unroll
           for (int h = 0; h < EC / 8; ++h) {
-            if (PFLAG(2)) { mq[8 * h] = 0.f; continue; }
+            if (PFLAG(2)) continue;
             float mn[8], cr[8];
             tmem_ld8(acc + 8 * h, mn);
             tmem_ld8(acc + BN + 8 * h, cr);
@@ -382,15 +447,13 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           if (lane == 0) mbar_arrive(&S.acc_empty[buf]);
           ++chunk;
         }
-        // output transform: Y_p +-= M'_q for the positions p with a nonzero coefficient
-        const char4 cf = *reinterpret_cast<const char4*>(S.coef[q]);
-        const int8_t cfa[4] = {cf.x, cf.y, cf.z, cf.w};
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          if (cfa[p] > 0) {
+          const uint32_t code = (cf >> (2 * p)) & 3u;
+          if (code == 1u) {
 #pragma unroll
             for (int j = 0; j < EC; ++j) Y[p][j] = __fadd_rn(Y[p][j], mq[j]);
-          } else if (cfa[p] < 0) {
+          } else if (code == 3u) {
 #pragma unroll
             for (int j = 0; j < EC; ++j) Y[p][j] = __fsub_rn(Y[p][j], mq[j]);
           }
@@ -437,10 +500,11 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
 #ifdef DWM_TC_PROFILE
   {
     // role r: 0 TMA (warp 12), 1 MMA (warp 13), 2 converter (warp 0), 3 epilogue (warp 4)
-    const int role = warp == WARP_TMA ? 0 : warp == WARP_MMA ? 1 : warp == 0 ? 2 : warp == 4 ? 3 : -1;
+    const int role = warp == WARP_TMA ? 0 : warp == WARP_MMA ? 1 : warp == 0 ? 2 : warp == EPI_WARP0 ? 3 : -1;
     if (role >= 0 && lane == 0) {
       atomicAdd(&g_tc_prof[role * 4 + 0], (unsigned long long)prof[0]);
       atomicAdd(&g_tc_prof[role * 4 + 1], (unsigned long long)prof[1]);
+      atomicAdd(&g_tc_prof[role * 4 + 2], (unsigned long long)prof[2]);
       atomicAdd(&g_tc_prof[role * 4 + 3], (unsigned long long)(clock64() - t_start));
     }
   }

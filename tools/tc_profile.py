@@ -32,9 +32,9 @@ R = U + (lib.dwm_filter_bytes(desc, 0, 2) + 255) // 256 * 256  # max|x| range sl
 _native.check(lib.dwm_conv2d_forward(desc, 0, 2, x.data_ptr(), w.data_ptr(), y.data_ptr(), V, ws_bytes,
                                      flag.data_ptr(), s))
 buf = (ctypes.c_ulonglong * 32)()
-names = ["TMA   wait b_empty", "MMA   wait acc_empty", "MMA   wait a_full", "CONV  wait b_full",
+names = ["VTMA  wait v_empty", "MMA   wait acc_empty", "MMA   wait a_full", "MMA   wait u_full", "CONV  wait v_full",
          "CONV  wait a_empty", "EPI   wait acc_full"]
-slots = [0, 4, 5, 8, 9, 12]
+slots = [0, 4, 5, 6, 8, 9, 12]
 for flags in [0, 1, 2, 4, 8, 1 | 2, 1 | 2 | 8, 1 | 2 | 4 | 8]:
     lib.dwm_debug_tc_flags(flags)
     lib.dwm_debug_tc_profile(buf, 1)
