@@ -193,7 +193,7 @@ template <int CHS>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_u,
                const float* __restrict__ inv_f, const uint32_t* __restrict__ xmax_slots, float* __restrict__ y,
-               int32_t* __restrict__ flag) {
+               int32_t* __restrict__ flag, int pf_all) {
   extern __shared__ uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -273,10 +273,12 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
                 for (int h = 0; h < na; ++h) tma_load_3d(S.v[s][h], &map_v, &S.v_full[s], SK * kc + VK * h, m0, q);
               }
               // V comes from HBM (the input transform just wrote it): prefetch
-              // the V box of stage it + V_PREFETCH into L2 -- once per m-block:
-              // the n_nblk CTAs of an m-block (running side by side) take turns
-              // by stage, so L2 sees no redundant prefetch requests
-              if (V_PREFETCH > 0 && !PFLAG(8) && (int)((it + V_PREFETCH) % n_nblk) == blk) {
+              // the V box of stage it + V_PREFETCH into L2.  pf_all == 0: once
+              // per m-block -- the n_nblk CTAs of an m-block (running side by
+              // side) take turns by stage, so L2 sees no redundant prefetch
+              // requests; pf_all == 1 (many-frequency plans, where the CTAs of
+              // an m-block drift further apart than L2 keeps V): every CTA
+              if (V_PREFETCH > 0 && !PFLAG(8) && (pf_all || (int)((it + V_PREFETCH) % n_nblk) == blk)) {
                 int nq = q, nk = kc + V_PREFETCH, nm = m0;
                 nq += nk / KS;
                 nk %= KS;
@@ -689,12 +691,22 @@ int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, i
   if (int st = device_sm_count(&sms)) return st;
   const int64_t items = ((d.tiles + BM - 1) / BM) * ((d.f + BN - 1) / BN);
   const int grid = (int)(items < sms ? items : sms);
+  // V prefetch by every CTA above this many frequencies: cfg4 11x11 (225
+  // frequencies) GEMM DRAM reads 52 -> 25 GB and 15.25 -> 14.86 ms at higher
+  // clocks (less DRAM power); turns win below: cfg4 9x9 (144) 8.9-9.2 vs
+  // 9.4-9.6 ms, 7x7 (100) 5.67 vs 6.15-6.22 ms (profiles/r2/ab_tc_prefetch_all.txt).
+  // DWM_TC_PF_ALL_Q overrides the threshold.
+  static const int pf_q = [] {
+    const char* e = getenv("DWM_TC_PF_ALL_Q");
+    return e ? atoi(e) : 200;
+  }();
+  const int pf_all = d.num_freqs > pf_q ? 1 : 0;
   if (tc_chunk_stages(d) == 2) {
     if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<2>, smem)) return st;
-    gemm_tc_kernel<2><<<grid, THREADS, smem, s>>>(d, mv, mu, inv_f, xmax, (float*)y, flag);
+    gemm_tc_kernel<2><<<grid, THREADS, smem, s>>>(d, mv, mu, inv_f, xmax, (float*)y, flag, pf_all);
   } else {
     if (int st = ensure_dynamic_smem((const void*)gemm_tc_kernel<1>, smem)) return st;
-    gemm_tc_kernel<1><<<grid, THREADS, smem, s>>>(d, mv, mu, inv_f, xmax, (float*)y, flag);
+    gemm_tc_kernel<1><<<grid, THREADS, smem, s>>>(d, mv, mu, inv_f, xmax, (float*)y, flag, pf_all);
   }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
