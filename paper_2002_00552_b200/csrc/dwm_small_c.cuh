@@ -457,7 +457,34 @@ __device__ __forceinline__ void ws_bar_wait(uint64_t* bar, uint32_t parity) {
                  : "memory");
 }
 
-template <class K>
+// Plan signatures the warp-specialized kernel is compiled for part by part
+// (square plans: the same tap-count sequence on both axes).  With the part
+// sequence known at compile time, each part's FMA chains, At stages and the
+// plan-order aggregation inline into one straight line: no runtime part
+// switch, and the y accumulators stay in the same registers across parts
+// (the generic loop moves them at every switch).  SIG 0 = generic.
+template <int SIG> struct PlanSig { static constexpr int n = 0; static constexpr int c[4] = {0, 0, 0, 0}; };
+template <> struct PlanSig<1> { static constexpr int n = 3; static constexpr int c[4] = {3, 1, 3, 0}; };  // 7x7/2
+// (the 16-part 11x11/4 sequence was measured slower unrolled: cfg3 1.32 -> 1.55 ms)
+template <int SIG>
+__host__ __device__ constexpr int sig_qoff(int p) {  // first frequency of part p (row-major parts)
+  int q = 0;
+  for (int i = 0; i < p; ++i) q += (PlanSig<SIG>::c[i / PlanSig<SIG>::n] + 1) * (PlanSig<SIG>::c[i % PlanSig<SIG>::n] + 1);
+  return q;
+}
+inline int match_plan_sig(const dwm_desc_t& d) {
+  auto axis_is = [&](const dwm_axis_part_t* parts, int n, auto sig) {
+    using S = decltype(sig);
+    if (n != S::n) return false;
+    for (int i = 0; i < n; ++i)
+      if (parts[i].count != S::c[i]) return false;
+    return true;
+  };
+  if (axis_is(d.row_parts, d.n_row_parts, PlanSig<1>{}) && axis_is(d.col_parts, d.n_col_parts, PlanSig<1>{})) return 1;
+  return 0;
+}
+
+template <class K, int SIG>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 small_c_ws_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* __restrict__ U,
                   float* __restrict__ y, int32_t* __restrict__ flag) {
@@ -507,8 +534,7 @@ small_c_ws_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* 
       ProdTile ptile[K::PPER];
 #pragma unroll
       for (int s = 0; s < K::PPER; ++s) ptile[s] = prod_tile(d, x, tb * BM + pt[s], pch[s]);
-      for (int p = 0; p < nparts; ++p, ++it) {
-        const int rp = p / d.n_col_parts, cp = p % d.n_col_parts;
+      auto produce = [&](int rp, int cp, auto store) {
         const uint32_t st = it % WS_STAGES;
         float win[K::PPER][4][4];
 #pragma unroll
@@ -517,14 +543,20 @@ small_c_ws_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* 
         ws_bar_wait(&empty[st], ((it / WS_STAGES) & 1) ^ 1);
         float* sV = sVbuf + st * K::VSTAGE;
 #pragma unroll
-        for (int s = 0; s < K::PPER; ++s) {
-          if (!pact[s]) continue;
-#define DWM_WSTS(A, B) transform_store<K, A, B>(win[s], sV, pt[s], pch[s])
-          DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cp].count, DWM_WSTS)
-#undef DWM_WSTS
-        }
+        for (int s = 0; s < K::PPER; ++s)
+          if (pact[s]) store(win[s], sV, pt[s], pch[s]);
         __syncwarp();
         if (lane == 0) ws_bar_arrive(&full[st]);
+        ++it;
+      };
+      // (the producer stays generic: its unrolled part sequence spilled at 48 registers)
+      for (int p = 0; p < nparts; ++p) {
+        const int rp = p / d.n_col_parts, cp = p % d.n_col_parts;
+        produce(rp, cp, [&](const float (&w)[4][4], float* sV, int t, int c) {
+#define DWM_WSTS(A, B) transform_store<K, A, B>(w, sV, t, c)
+          DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cp].count, DWM_WSTS)
+#undef DWM_WSTS
+        });
       }
     }
   } else {
@@ -534,19 +566,32 @@ small_c_ws_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* 
     f2 acc[TM][NP][2][2];
     uint32_t it = 0;
     for (int tb = blockIdx.x; tb < nblocks; tb += gridDim.x) {
-      int qoff = 0;
-      for (int p = 0; p < nparts; ++p, ++it) {
-        const int rp = p / d.n_col_parts, cpi = p % d.n_col_parts;
-        const uint32_t st = it % WS_STAGES;
-        ws_bar_wait(&full[st], (it / WS_STAGES) & 1);
-        const float* sV = sVbuf + st * K::VSTAGE;
-        const float* sUp = sU + qoff * CC * BN;
+      if constexpr (SIG == 0) {
+        int qoff = 0;
+        for (int p = 0; p < nparts; ++p, ++it) {
+          const int rp = p / d.n_col_parts, cpi = p % d.n_col_parts;
+          const uint32_t st = it % WS_STAGES;
+          ws_bar_wait(&full[st], (it / WS_STAGES) & 1);
+          const float* sV = sVbuf + st * K::VSTAGE;
+          const float* sUp = sU + qoff * CC * BN;
 #define DWM_WSC(A, B) consume_part_reg<K, A, B>(sV, sUp, acc, tm, tn, p == 0)
-        DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cpi].count, DWM_WSC)
+          DWM_PART_SWITCH(d.row_parts[rp].count, d.col_parts[cpi].count, DWM_WSC)
 #undef DWM_WSC
-        __syncwarp();
-        if (lane == 0) ws_bar_arrive(&empty[st]);
-        qoff += (d.row_parts[rp].count + 1) * (d.col_parts[cpi].count + 1);
+          __syncwarp();
+          if (lane == 0) ws_bar_arrive(&empty[st]);
+          qoff += (d.row_parts[rp].count + 1) * (d.col_parts[cpi].count + 1);
+        }
+      } else {
+        using S = PlanSig<SIG>;
+        static_for<S::n * S::n>([&](auto pI) {
+          constexpr int p = decltype(pI)::value, PR = S::c[p / S::n], PC = S::c[p % S::n];
+          const uint32_t st = it % WS_STAGES;
+          ws_bar_wait(&full[st], (it / WS_STAGES) & 1);
+          consume_part_reg<K, PR, PC>(sVbuf + st * K::VSTAGE, sU + sig_qoff<SIG>(p) * CC * BN, acc, tm, tn, p == 0);
+          __syncwarp();
+          if (lane == 0) ws_bar_arrive(&empty[st]);
+          ++it;
+        });
       }
       // epilogue: 2x2 tiles -> NCHW from the accumulator registers
       bool bad = false;
@@ -598,7 +643,14 @@ small_c_ws_kernel(const dwm_desc_t d, const float* __restrict__ x, const float* 
 template <class K>
 int launch_ws(const dwm_desc_t& d, const float* x, const float* U, float* y, int32_t* flag, cudaStream_t s) {
   const size_t smem = K::smem_bytes(d.num_freqs);
-  const void* kern = (const void*)small_c_ws_kernel<K>;
+  // plan-specialized kernels for RGB stems only (C_in = 3; compile time)
+  static const bool sig_off = getenv("DWM_SMALLC_NOSIG") != nullptr;  // (experiments)
+  constexpr bool sig_ok = K::CC == 3;
+  const int sig = (sig_off || !sig_ok) ? 0 : match_plan_sig(d);
+  const void* kern = (const void*)small_c_ws_kernel<K, 0>;
+  if constexpr (sig_ok) {
+    if (sig == 1) kern = (const void*)small_c_ws_kernel<K, 1>;
+  }
   if (int st = ensure_dynamic_smem(kern, smem)) return st;
   int sms = 0;
   if (int st = device_sm_count(&sms)) return st;
@@ -606,7 +658,13 @@ int launch_ws(const dwm_desc_t& d, const float* x, const float* U, float* y, int
   const int64_t nblocks = (d.tiles + K::BM - 1) / K::BM;
   int64_t gx = ((int64_t)sms + fblocks - 1) / fblocks;
   if (gx > nblocks) gx = nblocks;
-  small_c_ws_kernel<K><<<dim3((unsigned)gx, (unsigned)fblocks), WS_THREADS, smem, s>>>(d, x, U, y, flag);
+  const dim3 grid((unsigned)gx, (unsigned)fblocks);
+  if constexpr (sig_ok) {
+    if (sig == 1) small_c_ws_kernel<K, 1><<<grid, WS_THREADS, smem, s>>>(d, x, U, y, flag);
+    else small_c_ws_kernel<K, 0><<<grid, WS_THREADS, smem, s>>>(d, x, U, y, flag);
+  } else {
+    small_c_ws_kernel<K, 0><<<grid, WS_THREADS, smem, s>>>(d, x, U, y, flag);
+  }
   DWM_CUDA_TRY(cudaGetLastError());
   return DWM_OK;
 }
