@@ -186,6 +186,26 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
   });
 }
 
+// Division by a per-launch constant with a host-computed magic number
+// (q = (umulhi(n, m) + n) >> s, exact for 0 <= n < 2^31): the staging loop's
+// (channel, row, vector) decomposition ran on emulated integer division
+// (IABS/I2F/MUFU.RCP sequences were ~30 % of the kernel's instructions on cfg5).
+struct FastDiv {
+  uint32_t d, m, s;
+};
+static FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  while ((1u << f.s) < d) ++f.s;
+  f.m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << f.s) - d)) / d + 1);
+  return f;
+}
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+  return (int)((__umulhi((uint32_t)n, f.m) + (uint32_t)n) >> f.s);
+}
+struct ItDivs {
+  FastDiv nslots, wv, rpad, npad, nty;  // rows_staged*W/VEC, W/VEC, rows_staged*npad, npad, tile-row groups
+};
+
 #ifndef DWM_IT_MAXNREG
 #define DWM_IT_MAXNREG 56  // 5 CTAs of 224 threads per SM (tools/it_exp.sh); binary64 spills a little
 #endif
@@ -196,7 +216,8 @@ __device__ __forceinline__ void it_gather_part(const T* __restrict__ sc, const i
 template <typename T, bool WIDE, bool STREAM, int CB>
 __global__ void __maxnreg__(DWM_IT_MAXNREG)
 input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __restrict__ V, int rows_staged,
-                            int twb_arg, int ws_arg, int trows_arg, int n0, uint32_t* __restrict__ xmax) {
+                            int twb_arg, int ws_arg, int trows_arg, int n0, uint32_t* __restrict__ xmax,
+                            const ItDivs dv) {
   // WIDE == false: whole rows staged (ws == W, trows tile rows per CTA) -- the
   // common case, compiled without any of the column-block arithmetic
   const int twb = WIDE ? twb_arg : d.tw;
@@ -211,8 +232,12 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
   const int nxb = WIDE ? (d.tw + twb - 1) / twb : 1;
   const int tx0 = WIDE ? (int)(blockIdx.y % nxb) * twb : 0;
   const int nty = WIDE ? d.th : (d.th + trows - 1) / trows;
-  const int ty0 = WIDE ? (int)(blockIdx.y / nxb) % d.th : (int)(blockIdx.y % nty) * trows;
-  const int n = n0 + (WIDE ? (int)(blockIdx.y / (nxb * d.th)) : (int)(blockIdx.y / nty));  // image
+  // magic-number divisions in the non-streaming variants only: the streaming
+  // (many-frequency) ones measured 2-5 % slower with them (profiles/r2/ab_it_fastdiv.txt)
+  constexpr bool FD = !STREAM;
+  const int by_n = WIDE ? 0 : (FD ? fdiv((int)blockIdx.y, dv.nty) : (int)blockIdx.y / nty);  // image (whole-row CTAs)
+  const int ty0 = WIDE ? (int)(blockIdx.y / nxb) % d.th : ((int)blockIdx.y - by_n * nty) * trows;
+  const int n = n0 + (WIDE ? (int)(blockIdx.y / (nxb * d.th)) : by_n);
   const int cbase = WIDE ? 2 * tx0 * d.s_w - d.pad_left : -d.pad_left;  // input column of staged column 0
   const int c0 = blockIdx.x * CB;
   const int cb = min(CB, d.c - c0);
@@ -227,8 +252,8 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
     const int wv = d.w / VEC, nslots = rows_staged * wv, nitems = cb * nslots;
     const int npad = d.pad_left + d.pad_right;
     for (int p = threadIdx.x; p < cb * rows_staged * npad; p += blockDim.x) {
-      const int cc = p / (rows_staged * npad), rz = p - cc * rows_staged * npad;
-      const int r = rz / npad, z = rz - r * npad;
+      const int cc = FD ? fdiv(p, dv.rpad) : p / (rows_staged * npad), rz = p - cc * rows_staged * npad;
+      const int r = FD ? fdiv(rz, dv.npad) : rz / npad, z = rz - r * npad;
       sx[cc * pitch + r * ws + (z < d.pad_left ? z : d.w + z)] = T(0);
     }
 #ifndef DWM_IT_LOADS
@@ -241,8 +266,8 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int p = p0 + u * blockDim.x;
-        const int cc = p / nslots, rs = p - cc * nslots;
-        const int sr = rs / wv, scv = (rs - sr * wv) * VEC;
+        const int cc = FD ? fdiv(p, dv.nslots) : p / nslots, rs = p - cc * nslots;
+        const int sr = FD ? fdiv(rs, dv.wv) : rs / wv, scv = (rs - sr * wv) * VEC;
         const int row = row0 + sr;
         const bool ok = p < nitems && row >= 0 && row < d.h;
         q[u] = ok ? __ldg(reinterpret_cast<const float4*>(x + (((int64_t)n * d.c + c0 + cc) * d.h + row) * d.w + scv))
@@ -412,6 +437,11 @@ static int launch_input_smem_cb(const dwm_desc_t& d, const void* x, void* V, cud
   }
   const int nxb = (d.tw + twb - 1) / twb;
   const int nty = (d.th + trows - 1) / trows;
+  constexpr int VEC = 16 / sizeof(T);
+  const int npad = d.pad_left + d.pad_right;
+  const ItDivs dv{make_fastdiv((uint32_t)max(1, rows * (d.w / VEC))), make_fastdiv((uint32_t)max(1, d.w / VEC)),
+                  make_fastdiv((uint32_t)max(1, rows * npad)), make_fastdiv((uint32_t)max(1, npad)),
+                  make_fastdiv((uint32_t)nty)};
   // grid.y = images x CTAs per image must stay <= 65535: launch batch slices
   const int per_img = nty * nxb;
   if (per_img > 65535) return DWM_OK;  // (never at BASELINE sizes) the 1-D-grid kernel takes it
@@ -431,7 +461,7 @@ static int launch_input_smem_cb(const dwm_desc_t& d, const void* x, void* V, cud
   for (int n0 = 0; n0 < d.n; n0 += imgs_per_launch) {
     const int nb = min(imgs_per_launch, d.n - n0);
     const dim3 grid((unsigned)((d.c + CB - 1) / CB), (unsigned)(nb * per_img));
-    kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows, n0, xmax);
+    kern<<<grid, 32 * warps, smem, s>>>(d, (const T*)x, (T*)V, rows, twb, ws, trows, n0, xmax, dv);
     DWM_CUDA_TRY(cudaGetLastError());
   }
   *used = true;
