@@ -53,7 +53,8 @@ typedef enum dwm_dtype { DWM_F32 = 0, DWM_F64 = 1 } dwm_dtype;
  *            ascending GEMM, At.m.A row then column stage, plan-order part
  *            sum) over a V workspace.  Bit-identical to the reference where
  *            its BLAS accumulates sequentially (small C); f32 and f64.
- *   TC:      tcgen05/TMEM 3xTF32 GEMM with the output transform, part sum and
+ *   TC:      tcgen05/TMEM GEMM (3 fp16 products of power-of-two scaled
+ *            operands, FP32 accumulation) with the output transform, part sum and
  *            tile interleave fused in the epilogue (f32 only, C % 32 == 0;
  *            any F, in 64-filter blocks).
  *   SMALL_C: one fused kernel (input transform computed in shared memory,
@@ -137,7 +138,8 @@ int dwm_conv2d_small_c(const dwm_desc_t* desc, const void* x, const void* U,
 /* Cached-filter forward (the operator wrapper keeps U
  * per weight version; the reference recomputes G g G^T every call,
  * engines.py:246-248).  dwm_filter_bytes: bytes of U in the layout the
- * engine `algo` selects for this geometry (TC: hi|lo TF32 planes).  U depends
+ * engine `algo` selects for this geometry (TC: scaled fp16 hi|lo planes and
+ * per-filter scales).  U depends
  * only on (F, C, kernel, stride, algo), never on the batch or image size --
  * but the selected engine can, so prepare with the same desc as the forward.
  * dwm_conv2d_forward_prepared: the forward with U given; workspace holds V

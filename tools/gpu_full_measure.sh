@@ -17,6 +17,11 @@ for spec in "tc cfg4-11x11s1 gemm_tc" "it cfg4-11x11s1 input_transform" "it cfg5
   timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:$3 \
     -o $O/ncu_$1_$2 python tools/ncu_forward.py $2 > $O/ncu_$1_$2.log 2>&1
 done
+# summaries and the traffic table on the box, then drop the large reports
+# (gpurun copies back at most 64 MiB)
+for r in $O/ncu_*.ncu-rep; do python tools/ncu_summary.py $r > ${r%.ncu-rep}.txt 2>&1; done
+python tools/traffic_from_ncu.py $O $O/traffic.json > $O/traffic.txt 2>&1
+[ -n "$KEEP_REPS" ] || rm -f $O/ncu_*.ncu-rep
 for w in cfg1-5x5s1 cfg2-resnet50-stem cfg3-alexnet-conv1 cfg4-3x3s1 cfg4-5x5s1 cfg4-7x7s1 cfg4-9x9s1 cfg4-11x11s1 cfg5-3x3s2 cfg5-5x5s2; do
   timeout 300 python bench.py --workload $w --no-cpu-baseline --steps 10 > $O/bench_$w.json 2> $O/bench_$w.err
 done

@@ -3,7 +3,7 @@ captures of a measurement pass (tools/gpu_full_measure.sh): DRAM bytes per
 launch (dram__bytes_read.sum + dram__bytes_write.sum) per image, next to the
 kernel's compulsory bytes (the algorithmic bytes bench.py's roofline uses).
 
-    python tools/traffic_from_ncu.py gpurun_out/r2final
+    python tools/traffic_from_ncu.py gpurun_out/r2final [out.json]
 """
 import csv
 import json
@@ -40,7 +40,8 @@ def compulsory(kind, wl):
     y = 4.0 * wl.batch * wl.c_out * desc.oh * desc.ow
     v = 4.0 * desc.num_freqs * desc.tiles * wl.c_in
     u = 4.0 * desc.num_freqs * wl.c_out * wl.c_in
-    return {"tc": v + 2 * u + y, "it": x + v, "sc": x + u + y}[kind]
+    # tc: U is the stacked fp16 hi/lo split (2 x 2 bytes per fp32 value)
+    return {"tc": v + u + y, "it": x + v, "sc": x + u + y}[kind]
 
 
 def main():
@@ -61,7 +62,8 @@ def main():
             "note": ("writes below the compulsory bytes = dirty lines still in the 126 MB L2 at kernel end"
                      if m["dram__bytes_write.sum"] < comp and kind != "tc" else ""),
         }
-    (ROOT / "profiles" / "traffic.json").write_text(json.dumps(out, indent=1) + "\n")
+    dst = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "profiles" / "traffic.json"
+    dst.write_text(json.dumps(out, indent=1) + "\n")
     for name, ks in out.items():
         for k, e in ks.items():
             print(f"{name:22s} {k:16s} traffic/compulsory {e['traffic_over_compulsory']:.3f}")
