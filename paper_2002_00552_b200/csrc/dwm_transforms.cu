@@ -206,6 +206,15 @@ struct ItDivs {
   FastDiv nslots, wv, rpad, npad, nty;  // rows_staged*W/VEC, W/VEC, rows_staged*npad, npad, tile-row groups
 };
 
+// byte offset of the gather tables in the input transform's dynamic smem
+template <typename T>
+__host__ __device__ __forceinline__ size_t it_tab_offset(int cb, int pitch) {
+  return ((size_t)cb * pitch * sizeof(T) + 15) & ~(size_t)15;
+}
+__host__ __device__ __forceinline__ size_t it_tab_bytes(const dwm_desc_t& d, int twl, int trows) {
+  return (((size_t)d.n_col_parts * twl * 8 + 15) & ~(size_t)15) + (size_t)trows * d.n_row_parts * 16;
+}
+
 #ifndef DWM_IT_MAXNREG
 #define DWM_IT_MAXNREG 56  // 5 CTAs of 224 threads per SM (tools/it_exp.sh); binary64 spills a little
 #endif
@@ -304,6 +313,45 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
       }
     }
   }
+  // Gather offset tables (after the staged block): the staged-column offsets
+  // of the 4 window columns per (column part, tile column) and the
+  // staged-row offsets per (tile row, row part), -1 where the even extension
+  // truncates.  The values are the same for every channel lane, so the
+  // gather reads them (one broadcast LDS) instead of recomputing the
+  // predicates per tile and part (~30 % of the instructions on cfg5).
+  // (non-streaming variants only: the streaming ones measured slower with any
+  // change to this code, profiles/r2/ab_it_tables.txt)
+  constexpr bool TAB = !STREAM;
+  const int ncp = d.n_col_parts, nrp = d.n_row_parts;
+  const int twl = WIDE ? twb : d.tw;
+  short4* colsT = reinterpret_cast<short4*>(it_smem_raw + it_tab_offset<T>(CB, pitch));
+  int4* rowsT = reinterpret_cast<int4*>(it_smem_raw + it_tab_offset<T>(CB, pitch) + (((size_t)ncp * twl * 8 + 15) & ~(size_t)15));
+  for (int e = threadIdx.x; TAB && e < ncp * twl; e += blockDim.x) {
+    const int cp = e / twl, tx = tx0 + (e - cp * twl);
+    const dwm_axis_part_t Cc = d.col_parts[cp];
+    const int pc = Cc.count, lc = pc + 1;
+    short c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = 2 * tx + j;
+      const int col = Cc.origin + d.s_w * k - d.pad_left;  // staged columns cover every col read
+      c[j] = (short)((j < lc && k < d.ow - 1 + pc) ? col - cbase : -1);
+    }
+    colsT[e] = make_short4(c[0], c[1], c[2], c[3]);
+  }
+  for (int e = threadIdx.x; TAB && e < trows * nrp; e += blockDim.x) {
+    const int tyl = e / nrp, rp = e - tyl * nrp, ty = ty0 + tyl;
+    const dwm_axis_part_t R = d.row_parts[rp];
+    const int pr = R.count, lr = pr + 1;
+    int r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = 2 * ty + i;
+      const int rs = R.origin + d.s_h * (i + 2 * tyl);  // staged-row index (rows outside x are staged zeros)
+      r[i] = (i < lr && k < d.oh - 1 + pr) ? rs * ws : -1;
+    }
+    rowsT[e] = make_int4(r[0], r[1], r[2], r[3]);
+  }
   __syncthreads();
   if (xmax) xmax_reduce(amax, 0xffffffffu, xmax, blockIdx.x * 7 + blockIdx.y * 13 + threadIdx.x / 32);
 
@@ -323,25 +371,35 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
     int fq = 0;
     // even-extension truncation only reaches an odd last tile row / column
     const bool check = 2 * ty >= d.oh - 1 || 2 * tx >= d.ow - 1;
-    for (int rp = 0; rp < d.n_row_parts; ++rp) {
+    for (int rp = 0; rp < nrp; ++rp) {
       const dwm_axis_part_t R = d.row_parts[rp];
       const int pr = R.count, lr = pr + 1;
       int rows[4];
+      if constexpr (TAB) {
+        const int4 r4 = rowsT[tyl * nrp + rp];
+        rows[0] = r4.x, rows[1] = r4.y, rows[2] = r4.z, rows[3] = r4.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = 2 * ty + i;
-        const int rs = R.origin + d.s_h * (i + 2 * tyl);  // staged-row index (rows outside x are staged zeros)
-        rows[i] = (i < lr && k < d.oh - 1 + pr) ? rs * ws : -1;
+        for (int i = 0; i < 4; ++i) {
+          const int k = 2 * ty + i;
+          const int rs = R.origin + d.s_h * (i + 2 * tyl);  // staged-row index (rows outside x are staged zeros)
+          rows[i] = (i < lr && k < d.oh - 1 + pr) ? rs * ws : -1;
+        }
       }
-      for (int cp = 0; cp < d.n_col_parts; ++cp) {
+      for (int cp = 0; cp < ncp; ++cp) {
         const dwm_axis_part_t Cc = d.col_parts[cp];
         const int pc = Cc.count, lc = pc + 1;
         int cols[4];
+        if constexpr (TAB) {
+          const short4 c4 = colsT[cp * twl + (tx - tx0)];
+          cols[0] = c4.x, cols[1] = c4.y, cols[2] = c4.z, cols[3] = c4.w;
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = 2 * tx + j;
-          const int col = Cc.origin + d.s_w * k - d.pad_left;  // staged columns cover every col read
-          cols[j] = (j < lc && k < d.ow - 1 + pc) ? col - cbase : -1;
+          for (int j = 0; j < 4; ++j) {
+            const int k = 2 * tx + j;
+            const int col = Cc.origin + d.s_w * k - d.pad_left;  // staged columns cover every col read
+            cols[j] = (j < lc && k < d.ow - 1 + pc) ? col - cbase : -1;
+          }
         }
         T* vq = vout + (int64_t)fq * tc_stride;
         if (check) {
@@ -449,6 +507,8 @@ static int launch_input_smem_cb(const dwm_desc_t& d, const void* x, void* V, cud
   const bool stream = d.num_freqs > IT_STREAM_MIN_FREQS;
   auto kern = wide ? (stream ? input_transform_smem_kernel<T, true, true, CB> : input_transform_smem_kernel<T, true, false, CB>)
                    : (stream ? input_transform_smem_kernel<T, false, true, CB> : input_transform_smem_kernel<T, false, false, CB>);
+  // + the gather offset tables (non-streaming variants)
+  if (!stream) smem = it_tab_offset<T>(CB, rows * ws + 1) + it_tab_bytes(d, twb, trows);
   if (int st = ensure_dynamic_smem((const void*)kern, smem)) return st;
   // warps: a divisor of the tile-step count in [4, 8] so every warp gets the
   // same number of tiles (a warp step covers 32 / CB tiles)
