@@ -470,7 +470,7 @@ class GpuRunner:
         d = self.desc
         tc = self.engine == "tc"
         if tc:  # the engine's V range slots, as dwm_conv2d_forward keeps them after V and U
-            rng = torch.zeros(self._native.RANGE_BYTES // 4, dtype=torch.int32, device=self.x.device)
+            rng = torch.zeros(lib.dwm_range_bytes(d) // 4, dtype=torch.int32, device=self.x.device)
 
         def filt():
             check(lib.dwm_prepare_filter(d, F32, self.algo, self.w.data_ptr(), U, self.sptr))

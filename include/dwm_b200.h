@@ -119,12 +119,13 @@ int dwm_gemm_output(const dwm_desc_t* desc, int dtype, int algo, const void* V,
 
 /* The tcgen05 engine's range-carrying stage pair (what dwm_conv2d_forward
  * runs internally): dwm_input_transform_ranged is dwm_input_transform (f32)
- * that also records max|x| into `range` (DWM_RANGE_BYTES, device, 16-byte
- * aligned), from which dwm_gemm_output_tc picks the power-of-two V scale of
- * its fp16 split; U from dwm_prepare_filter(algo = DWM_ALGO_TC).
- * dwm_gemm_output with algo TC derives the range from V itself instead (one
- * more pass over V; workspace >= DWM_RANGE_BYTES). */
-#define DWM_RANGE_BYTES 512
+ * that also records each image's max|x| into `range` (dwm_range_bytes: one
+ * uint32 per image, device, 16-byte aligned), from which dwm_gemm_output_tc
+ * picks the per-image power-of-two V scale of its fp16 split; U from
+ * dwm_prepare_filter(algo = DWM_ALGO_TC).  dwm_gemm_output with algo TC
+ * derives the range from V itself instead (one more pass over V; workspace
+ * >= dwm_range_bytes). */
+size_t dwm_range_bytes(const dwm_desc_t* desc);
 int dwm_input_transform_ranged(const dwm_desc_t* desc, const void* x, void* V, uint32_t* range,
                                void* stream);
 int dwm_gemm_output_tc(const dwm_desc_t* desc, const void* V, const void* U, const uint32_t* range,

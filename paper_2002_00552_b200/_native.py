@@ -14,7 +14,6 @@ DWM_MAX_AXIS_PARTS = 16
 
 DWM_OK, DWM_EINVAL_SHAPE, DWM_EINVAL_DTYPE, DWM_NONFINITE, DWM_ECUDA, DWM_EUNSUPPORTED = range(6)
 DWM_F32, DWM_F64 = 0, 1
-RANGE_BYTES = 512  # DWM_RANGE_BYTES: the tcgen05 engine's max|x| slots
 DWM_ALGO_AUTO, DWM_ALGO_EXACT, DWM_ALGO_TC, DWM_ALGO_SMALL_C = 0, 1, 2, 3
 ALGOS = {"auto": DWM_ALGO_AUTO, "exact": DWM_ALGO_EXACT, "tc": DWM_ALGO_TC, "small_c": DWM_ALGO_SMALL_C}
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
@@ -23,7 +22,7 @@ ALGO_NAMES = {v: k for k, v in ALGOS.items()}
 EXPORTED_SYMBOLS = (
     "dwm_desc_init", "dwm_elementwise_count", "dwm_workspace_bytes", "dwm_select_algo",
     "dwm_filter_transform", "dwm_input_transform", "dwm_gemm_output", "dwm_input_transform_ranged",
-    "dwm_gemm_output_tc",
+    "dwm_gemm_output_tc", "dwm_range_bytes",
     "dwm_filter_bytes", "dwm_prepare_filter", "dwm_prepare_filter_strided", "dwm_conv2d_forward_prepared", "dwm_weight_grad_workspace_bytes", "dwm_weight_grad",
     "dwm_conv2d_small_c", "dwm_conv2d_forward", "dwm_last_error", "dwm_version",
 )
@@ -96,6 +95,8 @@ def load(required: bool = True):
     lib.dwm_input_transform.restype = I
     lib.dwm_gemm_output.argtypes = [D, I, I, P, P, P, P, P, S, P]
     lib.dwm_gemm_output.restype = I
+    lib.dwm_range_bytes.argtypes = [D]
+    lib.dwm_range_bytes.restype = ctypes.c_size_t
     lib.dwm_input_transform_ranged.argtypes = [D, P, P, P, P]
     lib.dwm_input_transform_ranged.restype = I
     lib.dwm_gemm_output_tc.argtypes = [D, P, P, P, P, P, P]

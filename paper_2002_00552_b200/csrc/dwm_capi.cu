@@ -181,8 +181,8 @@ size_t dwm_workspace_bytes(const dwm_desc_t* d, int dtype, int algo) {
   size_t u = (size_t)d->num_freqs * (size_t)d->f * (size_t)d->c * es;
   if (sel == DWM_ALGO_TC) u = tc_filter_bytes(*d);  // stacked, scaled fp16 hi/lo split of U
   const size_t v = sel == DWM_ALGO_SMALL_C ? 0 : v_bytes_of(d, es);
-  // TC: + the input transform's max|x| slots (after V and U)
-  return round_up(v, 256) + round_up(u, 256) + (sel == DWM_ALGO_TC ? DWM_XMAX_BYTES : 0);
+  // TC: + the input transform's per-image max|x| slots (after V and U)
+  return round_up(v, 256) + round_up(u, 256) + (sel == DWM_ALGO_TC ? xmax_bytes(*d) : 0);
 }
 
 // Workspace-type buffers (V, U, ws) are read with 16-byte vector loads and
@@ -235,6 +235,8 @@ int dwm_gemm_output(const dwm_desc_t* d, int dtype, int algo, const void* V, con
   }
   return launch_gemm_exact(*d, dtype, V, U, y, flag, (cudaStream_t)stream);
 }
+
+size_t dwm_range_bytes(const dwm_desc_t* d) { return d ? xmax_bytes(*d) : 0; }
 
 int dwm_input_transform_ranged(const dwm_desc_t* d, const void* x, void* V, uint32_t* range, void* stream) {
   if (int st = check_common(d, DWM_F32)) return st;
@@ -363,7 +365,7 @@ int dwm_conv2d_forward_prepared(const dwm_desc_t* d, int dtype, int algo, const 
     return launch_small_c(*d, x, U, y, flag, s);
   }
   const size_t vb = v_bytes_of(d, dtype == DWM_F64 ? 8 : 4);
-  const size_t need = sel == DWM_ALGO_TC ? round_up(vb, 256) + DWM_XMAX_BYTES : vb;
+  const size_t need = sel == DWM_ALGO_TC ? round_up(vb, 256) + xmax_bytes(*d) : vb;
   if (!ws || ws_bytes < need)
     return fail(DWM_EINVAL_SHAPE, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
   if ((st0 = check_aligned(ws, "workspace")) || (st0 = check_aligned(U, "U"))) return st0;

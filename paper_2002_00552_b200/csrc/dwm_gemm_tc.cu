@@ -17,9 +17,11 @@
 // sit in [2^12, 2^15) at their maxima: no fp16 overflow, and lo stays normal
 // down to 2^-26 of the maximum (MSE is absolute, so smaller values cost
 // nothing measurable):
-//   s_v = 2^(12 - floor(log2 max|x|))   |V| <= 4 max|x| (Bt rows: |.|-sums <= 2);
-//                                       max|x| from the input transform's
-//                                       staging loads (atomicMax slots)
+//   s_v = 2^(12 - floor(log2 max|x_n|)) per image n (|V| <= 4 max|x|: Bt rows
+//                                       have |.|-sums <= 2); max|x_n| from the
+//                                       input transform's staging loads
+//                                       (atomicMax per image), so an image's
+//                                       bits never depend on its batch-mates
 //   s_f = 2^(12 - floor(log2 max|w_f|)) |U_f| <= 2.25 max|w_f| (G: sums <= 1.5)
 // U'hi/U'lo come pre-split from the filter transform; V is scaled and split
 // on the fly by the converter warps.
@@ -122,7 +124,6 @@ struct __align__(1024) Smem {
   uint64_t a_full[A_SLOTS];         // converter -> MMA
   uint64_t acc_empty[2];            // epilogue -> MMA
   uint32_t tmem_base;
-  uint32_t xmax[2];                 // max|x| bits, reduced from the input transform's slots
   uint8_t coef[MAX_FREQS];           // output-transform sign of the 4 tile positions, 2 bits each
 };
 
@@ -217,11 +218,6 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     for (int i = 0; i < 2; ++i) mbar_init(&S.acc_empty[i], EPI_WARPS);
     fence_barrier_init();
   }
-  if (warp < 2) {  // max|x| over the input transform's DWM_XMAX_SLOTS slots
-    const uint32_t m = max(xmax_slots[tid], xmax_slots[tid + 64]);
-    const uint32_t r = __reduce_max_sync(0xffffffffu, m);
-    if (lane == 0) S.xmax[warp] = r;
-  }
   // output-transform coefficient of every frequency for the 4 tile positions
   for (int q = tid; q < Q; q += THREADS) {
     int rem = q, pr = 0, pc = 0, a = 0, b = 0;
@@ -246,7 +242,13 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
-  const int sv_exp = scale_exp(max(S.xmax[0], S.xmax[1]));
+  // per-image V scale exponent of tile row m of work item w (rows past the
+  // last tile take the last image's; they are computed but never stored)
+  const int64_t tiles_img = (int64_t)d.th * d.tw;
+  auto row_scale_exp = [&](int64_t w, int m) {
+    const int64_t t = min((w / n_nblk) * BM + m, d.tiles - 1);
+    return scale_exp(__ldg(xmax_slots + t / tiles_img));
+  };
 #ifdef DWM_TC_PROFILE
   long long prof[4] = {0, 0, 0, 0};
   const long long t_start = clock64();
@@ -351,9 +353,10 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * (warp % 4)) << 16);
     const int m = 32 * (warp % 4) + lane;
     const int h0 = CONV_WARPS == 8 ? warp / 4 : 0, hstep = CONV_WARPS == 8 ? 2 : 1;
-    const f2 sv2 = pk(exp2i(sv_exp), exp2i(sv_exp));
     uint32_t it = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const float sv = exp2i(row_scale_exp(w, m));
+      const f2 sv2 = pk(sv, sv);
       for (int q = 0; q < Q; ++q) {
         for (int kc = 0; kc < KS; ++kc, ++it) {
           const uint32_t sb = it % VSTAGES, sa = it % A_SLOTS;
@@ -409,9 +412,9 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
     const int c0 = ((warp - EPI_WARP0) / 4) * EC;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * quad) << 16);
     const int m = 32 * quad + lane;
-    const float inv_v = exp2i(-sv_exp);
     uint32_t it = 0, chunk = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const float inv_v = exp2i(-row_scale_exp(w, m));
       const int64_t tile = (w / n_nblk) * BM + m;
       const int n0 = (int)(w % n_nblk) * BN;
       float Y[4][EC];
@@ -516,14 +519,19 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
   if (warp == WARP_MMA) tmem_dealloc<512>(tmem);
 }
 
-// max|V| into the slots (the stage API's dwm_gemm_output gets V without the
-// input transform's max|x|; |V| itself is a valid bound for the scale)
-__global__ void v_absmax_kernel(const float* __restrict__ V, int64_t n, uint32_t* __restrict__ slots) {
-  uint32_t m = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    m = max(m, __float_as_uint(fabsf(V[i])));
-  m = __reduce_max_sync(0xffffffffu, m);
-  if (threadIdx.x % 32 == 0) atomicMax(slots + (blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32) % DWM_XMAX_SLOTS, m);
+// Per-image max|V| into the slots (the stage API's dwm_gemm_output gets V
+// without the input transform's max|x|; |V| itself is a valid bound for the
+// scale): one warp per (frequency, tile) row of C values.
+__global__ void v_absmax_kernel(const dwm_desc_t d, const float* __restrict__ V, uint32_t* __restrict__ slots) {
+  const int64_t rows = (int64_t)d.num_freqs * d.tiles, tiles_img = (int64_t)d.th * d.tw;
+  const int lane = threadIdx.x % 32;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x / 32) {
+    uint32_t m = 0;
+    for (int c = lane; c < d.c; c += 32) m = max(m, __float_as_uint(fabsf(V[r * d.c + c])));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) atomicMax(slots + (r % d.tiles) / tiles_img, m);
+  }
 }
 
 // Per-filter scale s_f = 2^(12 - floor(log2 max|w_f|)) (stored as 1 / s_f),
@@ -674,12 +682,11 @@ int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, i
   if (!tc_gemm_supported(d)) return fail(DWM_EUNSUPPORTED, "tcgen05 GEMM needs C %% 32 == 0");
   if (!xmax) {
     // no input-transform range: bound the scale by max|V| itself
-    if (!scratch || scratch_bytes < DWM_XMAX_BYTES)
-      return fail(DWM_EINVAL_SHAPE, "tcgen05 GEMM on a caller V needs %d bytes of workspace (got %zu)",
-                  (int)DWM_XMAX_BYTES, scratch_bytes);
-    DWM_CUDA_TRY(cudaMemsetAsync(scratch, 0, DWM_XMAX_BYTES, s));
-    const int64_t n = (int64_t)d.num_freqs * d.tiles * d.c;
-    v_absmax_kernel<<<1184, 256, 0, s>>>((const float*)V, n, (uint32_t*)scratch);
+    if (!scratch || scratch_bytes < xmax_bytes(d))
+      return fail(DWM_EINVAL_SHAPE, "tcgen05 GEMM on a caller V needs %zu bytes of workspace (4 per image, got %zu)",
+                  xmax_bytes(d), scratch_bytes);
+    DWM_CUDA_TRY(cudaMemsetAsync(scratch, 0, xmax_bytes(d), s));
+    v_absmax_kernel<<<1184, 256, 0, s>>>(d, (const float*)V, (uint32_t*)scratch);
     xmax = (const uint32_t*)scratch;
   }
   CUtensorMap mv, mu;

@@ -15,11 +15,11 @@ int launch_filter_transform(const dwm_desc_t& d, int dtype, const void* w, void*
 // [U'hi; U'lo] N = 128 B operand; then 1 / s_f per padded filter (fp32).
 int launch_filter_transform_f16split(const dwm_desc_t& d, const void* w, void* U, cudaStream_t s,
                                      const int64_t* strides = nullptr);
-// max|x| slots the float input transform fills when xmax != NULL (zeroed
-// first, on the same stream): the tcgen05 GEMM's V-scale bound
-constexpr int DWM_XMAX_SLOTS = 128;
-constexpr size_t DWM_XMAX_BYTES = DWM_XMAX_SLOTS * sizeof(uint32_t);
-static_assert(DWM_XMAX_BYTES == DWM_RANGE_BYTES, "C ABI range size");
+// max|x| per image (float bits, one uint32 slot per image) that the float
+// input transform fills when xmax != NULL (zeroed first, on the same stream):
+// the tcgen05 GEMM's per-image V-scale bound, so an image's result never
+// depends on the other images of the batch (chunking / sharding invariance)
+inline size_t xmax_bytes(const dwm_desc_t& d) { return ((size_t)d.n * sizeof(uint32_t) + 15) & ~(size_t)15; }
 int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* V, cudaStream_t s,
                            uint32_t* xmax = nullptr);
 int launch_gemm_exact(const dwm_desc_t& d, int dtype, const void* V, const void* U, void* y,
@@ -36,8 +36,8 @@ int launch_small_c(const dwm_desc_t& d, const void* x, const void* U, void* y, i
                    cudaStream_t s);
 bool tc_gemm_supported(const dwm_desc_t& d);
 size_t tc_filter_bytes(const dwm_desc_t& d);
-// xmax: the input transform's max|x| slots for V; NULL = bound by max|V|,
-// computed into scratch (>= DWM_XMAX_BYTES)
+// xmax: the input transform's per-image max|x| slots; NULL = bound by the
+// per-image max|V|, computed into scratch (>= xmax_bytes(d))
 int launch_gemm_tc(const dwm_desc_t& d, const void* V, const void* U, void* y, int32_t* flag, const uint32_t* xmax,
                    void* scratch, size_t scratch_bytes, cudaStream_t s);
 

@@ -51,12 +51,12 @@ __global__ void filter_transform_kernel(const dwm_desc_t d, const T* __restrict_
 // when it falls in the padding or past the part's strided slice
 // (k >= OUT-1+count: the reference's even-extension zeros, engines.py:109-115).
 // ---------------------------------------------------------------------------
-// max|x| of the staged input (the tcgen05 GEMM's operand-scale bound):
-// one atomicMax per warp into DWM_XMAX_SLOTS spread slots (float bits of a
+// max|x| of the staged input per image (the tcgen05 GEMM's operand-scale
+// bound): one atomicMax per warp into the image's slot (float bits of a
 // non-negative value order like unsigned integers).
-__device__ __forceinline__ void xmax_reduce(float amax, unsigned mask, uint32_t* xmax, unsigned spread) {
+__device__ __forceinline__ void xmax_reduce(float amax, unsigned mask, uint32_t* slot) {
   const uint32_t m = __reduce_max_sync(mask, __float_as_uint(amax));
-  if ((threadIdx.x % 32) == (unsigned)(__ffs(mask) - 1)) atomicMax(xmax + spread % DWM_XMAX_SLOTS, m);
+  if ((threadIdx.x % 32) == (unsigned)(__ffs(mask) - 1)) atomicMax(slot, m);
 }
 
 template <typename T>
@@ -132,7 +132,7 @@ __global__ void input_transform_kernel(const dwm_desc_t d, const T* __restrict__
       fq += lr * lc;
     }
   }
-  if (xmax) xmax_reduce(amax, __activemask(), xmax, (unsigned)(idx / 32));
+  if (xmax) atomicMax(xmax + n, __float_as_uint(amax));  // (fallback kernel: lanes may span images)
 }
 
 // ---------------------------------------------------------------------------
@@ -353,7 +353,7 @@ input_transform_smem_kernel(const dwm_desc_t d, const T* __restrict__ x, T* __re
     rowsT[e] = make_int4(r[0], r[1], r[2], r[3]);
   }
   __syncthreads();
-  if (xmax) xmax_reduce(amax, 0xffffffffu, xmax, blockIdx.x * 7 + blockIdx.y * 13 + threadIdx.x / 32);
+  if (xmax) xmax_reduce(amax, 0xffffffffu, xmax + n);
 
   constexpr int TPW = 32 / CB;  // tiles per warp step
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nwarps = blockDim.x / 32;
@@ -532,7 +532,7 @@ int launch_input_transform(const dwm_desc_t& d, int dtype, const void* x, void* 
                            uint32_t* xmax) {
   bool used = false;
   if (dtype == DWM_F64) xmax = nullptr;
-  if (xmax) DWM_CUDA_TRY(cudaMemsetAsync(xmax, 0, DWM_XMAX_BYTES, s));
+  if (xmax) DWM_CUDA_TRY(cudaMemsetAsync(xmax, 0, xmax_bytes(d), s));
   // 16-channel CTAs: DWM_IT_CB=16 (experiments) or the rule below
   static const int env_cb = [] {
     const char* e = getenv("DWM_IT_CB");

@@ -327,6 +327,35 @@ def _side_streams(dev):
     return _SIDE_STREAMS[dev]
 
 
+def _host_chunks(lib, desc, code, algo_code, n, dev):
+    """Chunk boundaries for the host-buffer forward.  The first chunk's H2D
+    and the last chunk's D2H are exposed, so chunks are small (about n/8) --
+    but each chunk is one launch of the persistent tcgen05 GEMM, whose work
+    items (128 tiles x 64 filters) run in waves of one per SM: a chunk that
+    fills 2.65 waves idles 12 % of the GEMM in its last wave.  For that
+    engine the smallest chunk size in [n/16, n/6] with the least wave
+    quantisation is picked (cfg4 11x11, N = 512: 48-image chunks = exactly
+    2 waves; cfg5, N = 1024: 72 images = 3 waves)."""
+    if n < 2:
+        return [0, n]
+    k = max(1, round(n / 8))
+    if lib.dwm_select_algo(desc, code, algo_code) == _native.DWM_ALGO_TC:
+        torch = _torch()
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        tiles_img = desc.tiles // desc.n
+        nblk = -(-desc.f // 64)
+
+        def waste(kk):
+            items = -(-kk * tiles_img // 128) * nblk
+            waves = -(-items // sms)
+            return waves * sms / items
+
+        cands = range(max(1, n // 16), max(2, n // 6) + 1)
+        k = min(cands, key=lambda kk: (round(waste(kk), 3), kk))
+    bounds = list(range(0, n, k)) + [n]
+    return bounds
+
+
 def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev):
     """Host-resident input/output: the batch is cut into chunks whose
     host->device copy, forward and device->host copy run on three streams, so
@@ -334,11 +363,7 @@ def _forward_host(lib, desc, code, algo_code, spec, x_h, w_d, y_h, flag, s, dev)
     independent, so chunking changes no result bit).  Runs with ``s`` current."""
     torch = _torch()
     n = x_h.shape[0]
-    # 8 chunks: the first H2D / last D2H chunk is exposed (1/8 of the
-    # transfer); 16 measured slower on cfg4 11x11 (32-image chunks fill 1.3
-    # waves of the persistent GEMM: 18.0k vs 20.2k images/s end to end)
-    chunks = 1 if n < 2 else min(8, n)
-    bounds = [round(i * n / chunks) for i in range(chunks + 1)]
+    bounds = _host_chunks(lib, desc, code, algo_code, n, dev)
     x_d = torch.empty(x_h.shape, dtype=x_h.dtype, device=dev)
     y_d = torch.empty(y_h.shape, dtype=y_h.dtype, device=dev)
     s_in, s_out = _side_streams(dev)

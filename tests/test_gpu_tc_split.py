@@ -1,14 +1,16 @@
 """GPU tests of the tcgen05 engine's fp16 split (csrc/dwm_gemm_tc.cu).
 
 The engine computes each FP32 contraction from three fp16 products of
-power-of-two scaled operands (V scaled by 2^(12 - floor(log2 max|x|)), U per
-filter by 2^(12 - floor(log2 max|w_f|))).  Properties checked here, on top of
+power-of-two scaled operands (V per image by 2^(12 - floor(log2 max|x_n|)),
+U per filter by 2^(12 - floor(log2 max|w_f|))).  Properties checked here, on top of
 the MSE-vs-reference bars every tc workload already passes (test_gpu_parity,
 test_gpu_acceptance):
   * the C-ABI stage pair (dwm_input_transform_ranged + dwm_gemm_output_tc)
     and dwm_gemm_output (range taken from V itself) give the forward's bits;
   * power-of-two scale invariance, bit for bit: y(2^a x, 2^b w) == 2^(a+b) y(x, w)
     far outside the fp16 range (the scales absorb it);
+  * per-image scales: each image's bits are those of the image run alone,
+    also when the batch mixes images of very different magnitudes;
   * one channel 2^20 larger than the rest (the shared V scale then puts the
     others' low parts near the fp16 subnormal range): MSE vs FP64 still at or
     below the reference DWM32's on the same data.
@@ -63,7 +65,7 @@ def test_stage_pair_and_self_ranged_gemm_match_forward(cuda, geom):
                     device="cuda")
     _native.check(lib.dwm_prepare_filter(desc, _native.DWM_F32, _native.DWM_ALGO_TC, w.data_ptr(), u.data_ptr(), s))
     v = torch.empty(desc.num_freqs * desc.tiles * desc.c, device="cuda")
-    rng = torch.zeros(_native.RANGE_BYTES // 4, dtype=torch.int32, device="cuda")
+    rng = torch.zeros(lib.dwm_range_bytes(desc) // 4, dtype=torch.int32, device="cuda")
     _native.check(lib.dwm_input_transform_ranged(desc, x.data_ptr(), v.data_ptr(), rng.data_ptr(), s))
     y2 = torch.full_like(y, float("nan"))
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -71,9 +73,10 @@ def test_stage_pair_and_self_ranged_gemm_match_forward(cuda, geom):
                                          flag.data_ptr(), s))
     # the stage API without a range: bound from max|V| (a different power of two, same bits)
     y3 = torch.full_like(y, float("nan"))
-    scratch = torch.empty(_native.RANGE_BYTES, dtype=torch.uint8, device="cuda")
+    rb = lib.dwm_range_bytes(desc)
+    scratch = torch.empty(rb, dtype=torch.uint8, device="cuda")
     _native.check(lib.dwm_gemm_output(desc, _native.DWM_F32, _native.DWM_ALGO_TC, v.data_ptr(), u.data_ptr(),
-                                      y3.data_ptr(), flag.data_ptr(), scratch.data_ptr(), _native.RANGE_BYTES, s))
+                                      y3.data_ptr(), flag.data_ptr(), scratch.data_ptr(), rb, s))
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
     assert torch.equal(y, y3)
@@ -102,3 +105,17 @@ def test_outlier_channel_accuracy(cuda):
     ref32 = dwm_conv2d_oracle(xn, wn, spec, np.float32)
     ours, theirs = mse(y, truth), mse(ref32, truth)
     assert ours <= theirs, (ours, theirs)
+
+
+def test_per_image_scale_independent_of_batch(cuda):
+    """Images of very different magnitudes in one batch: every image's output
+    is bit-identical to the image convolved alone (the V scale is per image)."""
+    lib = _native.load()
+    spec, desc, x, w = _setup((4, 128, 14, 64, 5, 1, 2), seed=3)
+    x[1] *= 2.0 ** 30
+    x[2] *= 2.0 ** -40
+    y = _forward(lib, x, w, spec, desc)
+    for i in range(4):
+        d1 = _native.make_desc(1, 128, 14, 14, 64, spec.kernel, spec.stride, spec.pad)
+        yi = _forward(lib, x[i:i + 1].contiguous(), w, spec, d1)
+        assert torch.equal(yi[0], y[i]), i
