@@ -84,7 +84,11 @@ constexpr int SK = 64;         // channels per pipeline stage (2 V atoms, 1 U at
 #define DWM_TC_VSTAGES 4
 #endif
 constexpr int VSTAGES = DWM_TC_VSTAGES;  // V ring: 32 KB stages, freed by the converter
-constexpr int STAGES = 4;      // U ring (16 KB stages) = commit ring, freed by the MMAs
+#ifndef DWM_TC_USTAGES
+#define DWM_TC_USTAGES 4
+#endif
+constexpr int USTAGES = DWM_TC_USTAGES;  // U ring (16 KB stages), freed by the MMAs
+constexpr int STAGES = 4;      // commit ring (done[]), one commit per stage; = A_SLOTS
 constexpr int A_SLOTS = 4;     // TMEM A ring: 4 x (hi 32 | lo 32) columns
 #ifndef DWM_TC_VPF
 #define DWM_TC_VPF 4
@@ -116,10 +120,10 @@ static_assert(32 * (CONV_WARPS * REG_CONV + 4 * REG_CTRL + EPI_WARPS * REG_EPI) 
 
 struct __align__(1024) Smem {
   float v[VSTAGES][2][BM * VK];     // [stage][atom][128 tiles][32 ch] fp32
-  uint16_t u[STAGES][2 * BN * SK];  // [stage][U'hi 64 rows; U'lo 64 rows][64 ch] fp16
+  uint16_t u[USTAGES][2 * BN * SK];  // [stage][U'hi 64 rows; U'lo 64 rows][64 ch] fp16
   uint64_t v_full[VSTAGES];         // V TMA -> converter
   uint64_t v_empty[VSTAGES];        // converter (V read) -> V TMA
-  uint64_t u_full[STAGES];          // U TMA -> MMA
+  uint64_t u_full[USTAGES];         // U TMA -> MMA
   uint64_t done[STAGES];            // MMA commit per stage -> U TMA, converter, epilogue
   uint64_t a_full[A_SLOTS];         // converter -> MMA
   uint64_t acc_empty[2];            // epilogue -> MMA
@@ -210,8 +214,8 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
       mbar_init(&S.v_full[i], 1);
       mbar_init(&S.v_empty[i], CONV_WARPS);
     }
+    for (int i = 0; i < USTAGES; ++i) mbar_init(&S.u_full[i], 1);
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&S.u_full[i], 1);
       mbar_init(&S.done[i], 1);
     }
     for (int i = 0; i < A_SLOTS; ++i) mbar_init(&S.a_full[i], CONV_WARPS);
@@ -302,8 +306,8 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
         const int blk = (int)(w % n_nblk);
         for (int q = 0; q < Q; ++q)
           for (int kc = 0; kc < KS; ++kc, ++it) {
-            const uint32_t s = it % STAGES;
-            if (it >= STAGES) mbar_wait(&S.done[s], ((it - STAGES) / STAGES) & 1);
+            const uint32_t s = it % USTAGES;
+            if (it >= USTAGES) mbar_wait(&S.done[(it - USTAGES) % STAGES], ((it - USTAGES) / STAGES) & 1);
             if (elect_one()) {
               // the U box is always full (channels past C are TMA zero fill)
               mbar_arrive_expect_tx(&S.u_full[s], U_ATOM_BYTES);
@@ -321,18 +325,18 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
       for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
         for (int q = 0; q < Q; ++q) {
           for (int kc = 0; kc < KS; ++kc, ++it) {
-            const uint32_t sb = it % STAGES, sa = it % A_SLOTS;
+            const uint32_t sb = it % STAGES, su = it % USTAGES, sa = it % A_SLOTS;
             const int na = stage_atoms(C, kc);
             const bool first = kc % CHS == 0;  // a chunk starts: fresh accumulators in buffer chunk % 2
             const uint32_t buf = chunk & 1u;
             if (first) PWAIT(0, &S.acc_empty[buf], ((chunk >> 1) & 1) ^ 1);
             PWAIT(1, &S.a_full[sa], (it / A_SLOTS) & 1);
-            PWAIT(2, &S.u_full[sb], (it / STAGES) & 1);
+            PWAIT(2, &S.u_full[su], (it / USTAGES) & 1);
             tc_fence_after();
             const uint32_t a_hi = tmem + COL_A + sa * A_COLS, a_lo = a_hi + A_COLS / 2;
             const uint32_t dacc = tmem + COL_ACC + buf * (2 * BN);
             if (elect_one()) {
-              const uint64_t du = sdesc_sw128(smem_u32(S.u[sb]));
+              const uint64_t du = sdesc_sw128(smem_u32(S.u[su]));
               for (int k = 0; k < 2 * na; ++k) {
                 // +32 B per K = 16 slice, in 16-byte descriptor units
                 mma_f16_ts(dacc, a_hi + 8 * k, du + 2 * k, idesc128, (first && k == 0) ? 0u : 1u);
