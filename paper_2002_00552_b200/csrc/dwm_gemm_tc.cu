@@ -112,8 +112,8 @@ constexpr uint32_t U_ATOM_BYTES = 2 * BN * SK * 2;  // 16 KB: [128 rows][64 fp16
 constexpr uint32_t COL_ACC = 0, COL_A = 256, A_COLS = 64;
 // setmaxnreg moves registers within the CTA's launch allocation (THREADS x the
 // compiled count: 128 at 512 threads, 96 at 640), so the budgets must fit it
-constexpr int REG_CONV = CONV_WARPS == 8 ? 40 : 72, REG_EPI = CONV_WARPS == 8 ? 184 : 192,
-              REG_CTRL = CONV_WARPS == 8 ? 32 : 56;
+constexpr int REG_CONV = CONV_WARPS == 8 ? 40 : 80, REG_EPI = CONV_WARPS == 8 ? 184 : 192,
+              REG_CTRL = CONV_WARPS == 8 ? 32 : 48;
 constexpr int REG_LAUNCH = CONV_WARPS == 8 ? 96 : 128;
 static_assert(32 * (CONV_WARPS * REG_CONV + 4 * REG_CTRL + EPI_WARPS * REG_EPI) <= THREADS * REG_LAUNCH,
               "register budgets exceed the launch allocation");
@@ -373,31 +373,29 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
           for (int h = h0; h < na; h += hstep) {
             if (PFLAG(1)) break;
             const uint32_t vrow = smem_u32(S.v[sb][h]);
+            // the atom's 32 channels of row m: all 8 loads first (the loads are
+            // volatile asm, so they would otherwise wait behind the previous
+            // group's tcgen05.st), then the split, then two 16-column stores
+            f2 xv[16];
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              uint32_t hi[8], lo[8];
+            for (int c8 = 0; c8 < 8; ++c8)
+              asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                           : "=l"(xv[2 * c8]), "=l"(xv[2 * c8 + 1])
+                           : "r"(vrow + sw128_offset(m, 4 * c8)));
+            uint32_t hi[16], lo[16];
 #pragma unroll
-              for (int c4 = 0; c4 < 4; ++c4) {
-                // row m, 16-byte chunk (4 hh + c4) of the SWIZZLE_128B tile: two
-                // channel pairs, scaled, split and packed with f32x2 / f16x2 ops
-                f2 x01, x23;
-                asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
-                             : "=l"(x01), "=l"(x23)
-                             : "r"(vrow + sw128_offset(m, 16 * hh + 4 * c4)));
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const float2 p = upk(mul2(e ? x23 : x01, sv2));
-                  const __half2 h = __float22half2_rn(p);
-                  const uint32_t hu = *reinterpret_cast<const uint32_t*>(&h);
-                  const __half2 l = __float22half2_rn(residual_f16x2(hu, p));
-                  hi[2 * c4 + e] = hu;
-                  lo[2 * c4 + e] = *reinterpret_cast<const uint32_t*>(&l);
-                }
-              }
-              // channels 32 h + 16 hh + [0, 16) -> columns 16 h + 8 hh + [0, 8)
-              tmem_st8u(base + 16 * h + 8 * hh, hi);
-              tmem_st8u(base + A_COLS / 2 + 16 * h + 8 * hh, lo);
+            for (int e = 0; e < 16; ++e) {
+              // a channel pair, scaled, split and packed with f32x2 / f16x2 ops
+              const float2 p = upk(mul2(xv[e], sv2));
+              const __half2 h2 = __float22half2_rn(p);
+              const uint32_t hu = *reinterpret_cast<const uint32_t*>(&h2);
+              const __half2 l2 = __float22half2_rn(residual_f16x2(hu, p));
+              hi[e] = hu;
+              lo[e] = *reinterpret_cast<const uint32_t*>(&l2);
             }
+            // channels 32 h + [0, 32) -> columns 16 h + [0, 16)
+            tmem_st16u(base + 16 * h, hi);
+            tmem_st16u(base + A_COLS / 2 + 16 * h, lo);
           }
           // every V value of the stage is in registers (consumed above): free the V slot
           __syncwarp();
