@@ -90,6 +90,9 @@ constexpr int VSTAGES = DWM_TC_VSTAGES;  // V ring: 32 KB stages, freed by the c
 constexpr int USTAGES = DWM_TC_USTAGES;  // U ring (16 KB stages), freed by the MMAs
 constexpr int STAGES = 4;      // commit ring (done[]), one commit per stage; = A_SLOTS
 constexpr int A_SLOTS = 4;     // TMEM A ring: 4 x (hi 32 | lo 32) columns
+#ifndef DWM_TC_U_EVICT_LAST
+#define DWM_TC_U_EVICT_LAST 0
+#endif
 #ifndef DWM_TC_VPF
 #define DWM_TC_VPF 4
 #endif
@@ -301,6 +304,9 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
       }
     } else if (warp == WARP_UTMA) {
       // ================= U TMA producer: [U'hi; U'lo] of (frequency, 64 channels, n-block) =================
+#if DWM_TC_U_EVICT_LAST
+      const uint64_t upol = l2_policy_evict_last();
+#endif
       uint32_t it = 0;
       for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
         const int blk = (int)(w % n_nblk);
@@ -311,7 +317,12 @@ gemm_tc_kernel(const dwm_desc_t d, const __grid_constant__ CUtensorMap map_v, co
             if (elect_one()) {
               // the U box is always full (channels past C are TMA zero fill)
               mbar_arrive_expect_tx(&S.u_full[s], U_ATOM_BYTES);
+#if DWM_TC_U_EVICT_LAST
+              // U is re-read by every m-block: keep it in L2 against the V stream
+              tma_load_2d_hint(S.u[s], &map_u, &S.u_full[s], SK * kc, (q * n_nblk + blk) * (2 * BN), upol);
+#else
               tma_load_2d(S.u[s], &map_u, &S.u_full[s], SK * kc, (q * n_nblk + blk) * (2 * BN));
+#endif
             }
             __syncwarp();
           }
