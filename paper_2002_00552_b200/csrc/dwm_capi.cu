@@ -240,6 +240,7 @@ size_t dwm_range_bytes(const dwm_desc_t* d) { return d ? xmax_bytes(*d) : 0; }
 
 int dwm_input_transform_ranged(const dwm_desc_t* d, const void* x, void* V, uint32_t* range, void* stream) {
   if (int st = check_common(d, DWM_F32)) return st;
+  if (!range) return fail(DWM_EINVAL_SHAPE, "range pointer is NULL (dwm_range_bytes(desc) bytes of device memory)");
   if (int st = check_aligned(V, "V")) return st;
   if (int st = check_aligned(range, "range")) return st;
   return launch_input_transform(*d, DWM_F32, x, V, (cudaStream_t)stream, range);
@@ -248,6 +249,7 @@ int dwm_input_transform_ranged(const dwm_desc_t* d, const void* x, void* V, uint
 int dwm_gemm_output_tc(const dwm_desc_t* d, const void* V, const void* U, const uint32_t* range, void* y,
                        int32_t* flag, void* stream) {
   if (int st = check_common(d, DWM_F32)) return st;
+  if (!range) return fail(DWM_EINVAL_SHAPE, "range pointer is NULL (fill it with dwm_input_transform_ranged)");
   if (int st = check_aligned(V, "V")) return st;
   if (int st = check_aligned(U, "U")) return st;
   if (int st = check_aligned(range, "range")) return st;

@@ -96,3 +96,22 @@ def test_workspace_pointers_must_be_16_byte_aligned():
     assert st == _native.DWM_EINVAL_SHAPE and "16-byte aligned" in _native.last_error()
     st = lib.dwm_input_transform(d, _native.DWM_F32, 0x1000, 0x1008, None)
     assert st == _native.DWM_EINVAL_SHAPE
+
+
+def test_range_stage_api_validation():
+    """The tcgen05 range-carrying stage pair: one uint32 max|x| slot per image
+    (16-byte rounded), a NULL or misaligned range is rejected before any
+    launch (no device needed)."""
+    from paper_2002_00552_b200 import _native
+    lib = _native.load()
+    d = _native.make_desc(5, 64, 8, 8, 64, (3, 3), (1, 1), (1, 1, 1, 1))
+    assert lib.dwm_range_bytes(d) == 32  # 5 images x 4 bytes, rounded to 16
+    st = lib.dwm_input_transform_ranged(d, 0x1000, 0x2000, None, None)
+    assert st == _native.DWM_EINVAL_SHAPE and "range" in _native.last_error()
+    st = lib.dwm_input_transform_ranged(d, 0x1000, 0x2000, 0x3004, None)
+    assert st == _native.DWM_EINVAL_SHAPE and "16-byte aligned" in _native.last_error()
+    st = lib.dwm_gemm_output_tc(d, 0x2000, 0x3000, None, 0x4000, None, None)
+    assert st == _native.DWM_EINVAL_SHAPE and "range" in _native.last_error()
+    # the forward's workspace holds V, U and the range slots
+    ws = lib.dwm_workspace_bytes(d, _native.DWM_F32, _native.DWM_ALGO_TC)
+    assert ws >= 4 * d.num_freqs * d.tiles * 64 + lib.dwm_filter_bytes(d, _native.DWM_F32, _native.DWM_ALGO_TC) + 32
