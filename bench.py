@@ -413,7 +413,10 @@ class GpuRunner:
         self.working_set = self.x_bytes + self.y_bytes + self.v_bytes
         self.flush = (torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
                       if self.working_set < 4 * L2_BYTES else None)
-        self.launches_per_step = 2 if self.engine == "small_c" else 3
+        # our kernels per dwm_conv2d_forward: small-C = filter transform + fused
+        # kernel; tc = filter scale + filter split + input transform + GEMM (the
+        # range-slot memset is a driver memset, not counted); exact = 3
+        self.launches_per_step = {"small_c": 2, "tc": 4}.get(self.engine, 3)
 
     def step(self):
         st = self.lib.dwm_conv2d_forward(self.desc, self._native.DWM_F32, self.algo, self.x.data_ptr(),
