@@ -730,6 +730,8 @@ def make_roofline(stage_ms, run, peaks):
             # three fp16 tensor products (hi*hi + hi*lo + lo*hi) per fp32 MAC
             k["tensor_tflops_3xf16"] = 3 * gemm_flops / (ms * 1e-3) / 1e12
             k["tensor_frac"] = k["tensor_tflops_3xf16"] / peaks["bf16_tflops"]
+            # the round-1 3xTF32 denominator, for comparison across rounds
+            k["tensor_frac_vs_tf32_peak"] = k["tensor_tflops_3xf16"] / peaks["tf32_tflops"]
         if name == "conv2d_small_c":
             k["fp32_tflops"] = small_c_fp32_ops(desc) / (ms * 1e-3) / 1e12
             k["fp32_frac"] = k["fp32_tflops"] / peaks["fp32_tflops"]
